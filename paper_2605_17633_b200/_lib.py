@@ -1,0 +1,76 @@
+"""ctypes binding of ``libzstripe_b200.so`` (the C ABI in ``include/zstripe_b200.h``).
+
+This module is the only place Python touches the native library.  It fails
+loudly: a missing or stale library raises at import of the first op, and
+every non-zero ``zs_status`` becomes a ``RuntimeError`` carrying the
+library's own status string.  There is no CPU fallback anywhere.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "_lib" / "libzstripe_b200.so"
+
+_p = C.c_void_p
+_i = C.c_int
+_ll = C.c_longlong
+_f = C.c_float
+
+# name -> argtypes (restype is c_int unless noted)
+SIGNATURES: dict[str, list] = {
+    "zs_abi_version": [],
+    "zs_sobel_saliency": [_p, _i, _i, _i, _i, _i, _p, _p, _p],
+    "zs_rank_order": [_p, _i, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p],
+    "zs_permute_rows_f32": [_p, _p, _p, _ll, _i, _p],
+    "zs_permute_rows_bf16": [_p, _p, _p, _ll, _i, _p],
+    "zs_layout_maps": [_p, _p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p],
+    "zs_prefix_keep_rows": [_i, _i, _i, _p, _p, _p, _p],
+    "zs_layernorm_rows": [_p, _ll, _p, _ll, _i, _p, _p, _f, _p, _ll, _i, _p],
+    "zs_gemm_bf16": [_i, _p, _ll, _p, _ll, _i, _i, _i, _p, _p, _ll, _p, _ll, _p, _p, _i, _p, _p],
+    "zs_stripe_attn_fwd": [_p, _p, _p, _ll, _ll, _ll, _ll, _ll, _i, _i, _i, _i, _i, _p, _p, _i, _p, _p, _i, _i,
+                           _i, _f, _p, _ll, _ll, _p],
+    "zs_rc_mlp_fwd": [_p, _ll, _p, _i, _p, _i, _i, _p, _p, _f, _p, _p, _p, _p, _i, _p, _i, _p, _p],
+    "zs_patchify": [_p, _i, _i, _i, _i, _i, _p, _p],
+    "zs_im2col3x3": [_p, _i, _i, _i, _i, _p, _p],
+}
+
+_lib: C.CDLL | None = None
+
+
+def load() -> C.CDLL:
+    """Load (once) and type the native library; raise if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback for the B200 kernels)"
+        )
+    lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | getattr(os, "RTLD_LOCAL", 0))
+    lib.zs_status_string.restype = C.c_char_p
+    lib.zs_status_string.argtypes = [_i]
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = _i
+    _lib = lib
+    return lib
+
+
+def exported_symbols() -> list[str]:
+    return ["zs_status_string", *SIGNATURES.keys()]
+
+
+def status_string(rc: int) -> str:
+    return load().zs_status_string(rc).decode()
+
+
+def call(name: str, *args) -> None:
+    rc = getattr(load(), name)(*args)
+    if rc != 0:
+        raise RuntimeError(f"{name} failed: zs_status {rc} ({status_string(rc)})")

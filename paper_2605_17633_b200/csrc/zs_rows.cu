@@ -1,0 +1,360 @@
+// zs_rows.cu — HBM-bound row kernels of the hot path: layernorm (+gather),
+// row permutation (window partition / σ / layout switches), layout maps,
+// prefix keep-set compaction, and the SAM-frame im2col helpers.
+//
+// All of these are pure data movement or per-row reductions: one warp per
+// row, 16-byte vector accesses, grids sized as a multiple of the SM count.
+#include "zs_common.cuh"
+#include "zs_host.h"
+
+namespace zs {
+
+// ------------------------------------------------------------------ layernorm
+// Two-pass per-row LN with population variance (tensor.py:214-236):
+//   mean = sum(x)/C; c = x - mean; var = sum(c*c)/C; y = c * (1/sqrt(var+eps)) * g + b
+template <bool OUT_F32>
+__global__ void __launch_bounds__(256) ln_rows_kernel(const float* __restrict__ x, long long ldx,
+                                                      const int* __restrict__ rows,
+                                                      const int* __restrict__ out_rows, long long n,
+                                                      const int* __restrict__ n_dev, int C,
+                                                      const float* __restrict__ g, const float* __restrict__ b,
+                                                      float eps, void* out, long long ldo) {
+  constexpr int MAXV = 16;  // C <= 2048
+  long long nn = n;
+  if (n_dev) nn = min((long long)*n_dev, n);
+  const int lane = threadIdx.x & 31;
+  const int C4 = C >> 2;
+  for (long long i = (long long)blockIdx.x * 8 + (threadIdx.x >> 5); i < nn; i += (long long)gridDim.x * 8) {
+    const long long src = rows ? (long long)rows[i] : i;
+    const long long dst = out_rows ? (long long)out_rows[i] : i;
+    const float4* xr = reinterpret_cast<const float4*>(x + src * ldx);
+    float4 v[MAXV];
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < MAXV; ++j) {
+      const int c = lane + 32 * j;
+      if (c < C4) {
+        v[j] = xr[c];
+        s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+      } else {
+        v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float mean = s / (float)C;
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < MAXV; ++j) {
+      const int c = lane + 32 * j;
+      if (c < C4) {
+        v[j].x -= mean;
+        v[j].y -= mean;
+        v[j].z -= mean;
+        v[j].w -= mean;
+        q += (v[j].x * v[j].x + v[j].y * v[j].y) + (v[j].z * v[j].z + v[j].w * v[j].w);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    const float inv = 1.0f / sqrtf(q / (float)C + eps);
+#pragma unroll
+    for (int j = 0; j < MAXV; ++j) {
+      const int c = lane + 32 * j;
+      if (c < C4) {
+        const float4 gg = __ldg(reinterpret_cast<const float4*>(g) + c);
+        const float4 bb = __ldg(reinterpret_cast<const float4*>(b) + c);
+        float4 y;
+        y.x = v[j].x * inv * gg.x + bb.x;
+        y.y = v[j].y * inv * gg.y + bb.y;
+        y.z = v[j].z * inv * gg.z + bb.z;
+        y.w = v[j].w * inv * gg.w + bb.w;
+        if constexpr (OUT_F32) {
+          reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + dst * ldo)[c] = y;
+        } else {
+          uint2 w;
+          w.x = pack_bf16(y.x, y.y);
+          w.y = pack_bf16(y.z, y.w);
+          reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + dst * ldo)[c] = w;
+        }
+      }
+    }
+  }
+}
+
+static int grid_for_rows(long long rows, int rows_per_cta) {
+  long long g = (rows + rows_per_cta - 1) / rows_per_cta;
+  const long long cap = (long long)num_sms() * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+int launch_layernorm(const float* x, long long ldx, const int* rows, const int* out_rows, long long n,
+                     const int* n_dev, int C, const float* g, const float* b, float eps, void* out, long long ldo,
+                     int out_f32, cudaStream_t st) {
+  if (n <= 0) return 0;
+  if (!x || !g || !b || !out) return ZS_ERR_ARG;
+  if (C <= 0 || C % 4 || C > 2048 || ldx % 4 || (out_f32 ? ldo % 4 : ldo % 4)) return ZS_ERR_SHAPE;
+  const int grid = grid_for_rows(n, 8);
+  if (out_f32)
+    ln_rows_kernel<true><<<grid, 256, 0, st>>>(x, ldx, rows, out_rows, n, n_dev, C, g, b, eps, out, ldo);
+  else
+    ln_rows_kernel<false><<<grid, 256, 0, st>>>(x, ldx, rows, out_rows, n, n_dev, C, g, b, eps, out, ldo);
+  return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
+}
+
+// ------------------------------------------------------------------ permute
+template <typename V>
+__global__ void __launch_bounds__(256) permute_rows_kernel(const V* __restrict__ src, V* __restrict__ dst,
+                                                           const int* __restrict__ map, long long rows,
+                                                           int nvec) {
+  const int lane = threadIdx.x & 31;
+  for (long long r = (long long)blockIdx.x * 8 + (threadIdx.x >> 5); r < rows; r += (long long)gridDim.x * 8) {
+    const int s = map[r];
+    V* d = dst + r * nvec;
+    if (s >= 0) {
+      const V* a = src + (long long)s * nvec;
+      for (int c = lane; c < nvec; c += 32) d[c] = a[c];
+    } else {
+      V z;
+      memset(&z, 0, sizeof(V));
+      for (int c = lane; c < nvec; c += 32) d[c] = z;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ layout maps
+__global__ void maps_local_kernel(const int* __restrict__ sig_loc, int B, int H, int W, int win, int nwx, int nwin,
+                                  int* l_from_s, int* s_from_l, unsigned char* l_is_pad) {
+  const long long S2 = (long long)win * win;
+  const long long total = (long long)B * nwin * S2;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < total;
+       r += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(r % S2);
+    const long long bw = r / S2;
+    const int w = (int)(bw % nwin);
+    const int b = (int)(bw / nwin);
+    const int t = sig_loc[r];
+    const int y = (w / nwx) * win + t / win;
+    const int x = (w % nwx) * win + t % win;
+    (void)i;
+    if (y < H && x < W) {
+      const int s = b * H * W + y * W + x;
+      if (l_from_s) l_from_s[r] = s;
+      if (s_from_l) s_from_l[s] = (int)r;
+      if (l_is_pad) l_is_pad[r] = 0;
+    } else {
+      if (l_from_s) l_from_s[r] = -1;
+      if (l_is_pad) l_is_pad[r] = 1;
+    }
+  }
+}
+__global__ void maps_global_kernel(const int* __restrict__ sig_glob, int B, int HW, int* s_from_g) {
+  const long long total = (long long)B * HW;
+  for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
+       g += (long long)gridDim.x * blockDim.x) {
+    const int b = (int)(g / HW);
+    s_from_g[(long long)b * HW + sig_glob[g]] = (int)g;
+  }
+}
+__global__ void maps_cross_kernel(const int* __restrict__ sig_glob, int B, int HW, long long nl,
+                                  const int* __restrict__ s_from_l, const int* __restrict__ s_from_g,
+                                  const int* __restrict__ l_from_s, int* g_from_l, int* l_from_g) {
+  const long long ng = (long long)B * HW;
+  const long long total = ng > nl ? ng : nl;
+  for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < total;
+       r += (long long)gridDim.x * blockDim.x) {
+    if (r < ng && g_from_l) {
+      const int b = (int)(r / HW);
+      g_from_l[r] = s_from_l[(long long)b * HW + sig_glob[r]];
+    }
+    if (r < nl && l_from_g) {
+      const int s = l_from_s[r];
+      l_from_g[r] = s >= 0 ? s_from_g[s] : -1;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ keep rows
+// counts[u] = # non-pad rows among the first K rows of unit u
+__global__ void keep_count_kernel(int U, int S, int K, const unsigned char* __restrict__ is_pad, int* counts) {
+  const int lane = threadIdx.x & 31;
+  for (int u = blockIdx.x * 8 + (threadIdx.x >> 5); u < U; u += gridDim.x * 8) {
+    int c = 0;
+    for (int i = lane; i < K; i += 32) c += is_pad ? (is_pad[(long long)u * S + i] == 0) : 1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) counts[u] = c;
+  }
+}
+// In-place exclusive scan of counts[0..U) by one CTA; counts[U] = total.
+__global__ void __launch_bounds__(1024) keep_scan_kernel(int U, int* counts) {
+  __shared__ int warp_sums[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = 0; base < U; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int v = i < U ? counts[i] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_sums[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      int ws = warp_sums[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, ws, o);
+        if (lane >= o) ws += t;
+      }
+      warp_sums[lane] = ws;
+    }
+    __syncthreads();
+    const int excl = carry + (wid ? warp_sums[wid - 1] : 0) + incl - v;
+    if (i < U) counts[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += warp_sums[31];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) counts[U] = carry;
+}
+__global__ void keep_write_kernel(int U, int S, int K, const unsigned char* __restrict__ is_pad,
+                                  const int* __restrict__ offsets, int* keep_rows) {
+  const int lane = threadIdx.x & 31;
+  for (int u = blockIdx.x * 8 + (threadIdx.x >> 5); u < U; u += gridDim.x * 8) {
+    int pos = offsets[u];
+    for (int i0 = 0; i0 < K; i0 += 32) {
+      const int i = i0 + lane;
+      const long long r = (long long)u * S + i;
+      const bool keep = i < K && (!is_pad || is_pad[r] == 0);
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (keep) keep_rows[pos + __popc(m & ((1u << lane) - 1u))] = (int)r;
+      pos += __popc(m);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ SAM frame
+__global__ void patchify_kernel(const float* __restrict__ img, int B, int Cin, int H, int W, int P,
+                                __nv_bfloat16* __restrict__ out) {
+  const int gh = H / P, gw = W / P;
+  const long long ncol = (long long)Cin * P * P;
+  const long long total = (long long)B * gh * gw * ncol;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long row = e / ncol;
+    const int col = (int)(e % ncol);
+    const int c = col / (P * P), ky = (col / P) % P, kx = col % P;
+    const int b = (int)(row / (gh * gw));
+    const int t = (int)(row % (gh * gw));
+    const int y = (t / gw) * P + ky, x = (t % gw) * P + kx;
+    out[e] = __float2bfloat16_rn(img[(((long long)b * Cin + c) * H + y) * W + x]);
+  }
+}
+__global__ void im2col3x3_kernel(const __nv_bfloat16* __restrict__ x, int B, int H, int W, int C,
+                                 __nv_bfloat16* __restrict__ out) {
+  const long long ncol = 9LL * C;
+  const long long total = (long long)B * H * W * ncol;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long row = e / ncol;
+    const int col = (int)(e % ncol);
+    const int c = col / 9, ky = (col / 3) % 3, kx = col % 3;
+    const int b = (int)(row / (H * W));
+    const int t = (int)(row % (H * W));
+    const int y = t / W + ky - 1, xx = t % W + kx - 1;
+    __nv_bfloat16 v = __float2bfloat16_rn(0.f);
+    if (y >= 0 && y < H && xx >= 0 && xx < W) v = x[(((long long)b * H + y) * W + xx) * C + c];
+    out[e] = v;
+  }
+}
+
+}  // namespace zs
+
+// ================================================================== C ABI
+using namespace zs;
+
+static inline cudaStream_t S(zs_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" int zs_layernorm_rows(const float* x, long long ldx, const int32_t* rows, long long n, int C,
+                                 const float* gamma, const float* beta, float eps, void* out, long long ldo,
+                                 int out_f32, zs_stream_t stream) {
+  return launch_layernorm(x, ldx, rows, nullptr, n, nullptr, C, gamma, beta, eps, out, ldo, out_f32, S(stream));
+}
+
+extern "C" int zs_permute_rows_f32(const float* src, float* dst, const int32_t* map, long long rows_out, int C,
+                                   zs_stream_t stream) {
+  if (rows_out <= 0) return 0;
+  if (!src || !dst || !map) return ZS_ERR_ARG;
+  if (C <= 0 || C % 4) return ZS_ERR_SHAPE;
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) return ZS_ERR_ALIGN;
+  permute_rows_kernel<float4><<<grid_for_rows(rows_out, 8), 256, 0, S(stream)>>>(
+      reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), map, rows_out, C / 4);
+  return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
+}
+
+extern "C" int zs_permute_rows_bf16(const void* src, void* dst, const int32_t* map, long long rows_out, int C,
+                                    zs_stream_t stream) {
+  if (rows_out <= 0) return 0;
+  if (!src || !dst || !map) return ZS_ERR_ARG;
+  if (C <= 0 || C % 8) return ZS_ERR_SHAPE;
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) return ZS_ERR_ALIGN;
+  permute_rows_kernel<uint4><<<grid_for_rows(rows_out, 8), 256, 0, S(stream)>>>(
+      reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), map, rows_out, C / 8);
+  return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
+}
+
+extern "C" int zs_layout_maps(const int32_t* sigma_glob, const int32_t* sigma_loc, int B, int H, int W, int window,
+                              int32_t* l_from_s, int32_t* g_from_l, int32_t* l_from_g, int32_t* s_from_g,
+                              int32_t* s_from_l, uint8_t* l_is_pad, zs_stream_t stream) {
+  if (B <= 0 || H <= 0 || W <= 0 || window <= 0) return ZS_ERR_SHAPE;
+  const int nwy = (H + window - 1) / window, nwx = (W + window - 1) / window;
+  const int nwin = nwy * nwx;
+  const long long nl = (long long)B * nwin * window * window;
+  const int HW = H * W;
+  const int grid = num_sms() * 4;
+  if ((g_from_l || l_from_g) && (!sigma_glob || !sigma_loc || !s_from_l || !s_from_g || !l_from_s))
+    return ZS_ERR_ARG;
+  if (sigma_loc) maps_local_kernel<<<grid, 256, 0, S(stream)>>>(sigma_loc, B, H, W, window, nwx, nwin, l_from_s,
+                                                                 s_from_l, l_is_pad);
+  if (sigma_glob && s_from_g) maps_global_kernel<<<grid, 256, 0, S(stream)>>>(sigma_glob, B, HW, s_from_g);
+  if (g_from_l || l_from_g)
+    maps_cross_kernel<<<grid, 256, 0, S(stream)>>>(sigma_glob, B, HW, nl, s_from_l, s_from_g, l_from_s, g_from_l,
+                                                    l_from_g);
+  return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
+}
+
+// keep_rows must hold U*K entries; unit_offsets must hold U+1 entries and
+// receives the exclusive prefix of per-unit kept counts (total at [U]).
+extern "C" int zs_prefix_keep_rows(int U, int S_, int K, const uint8_t* is_pad, int32_t* keep_rows,
+                                   int32_t* unit_offsets, zs_stream_t stream) {
+  if (U <= 0) return 0;
+  if (K <= 0 || K > S_ || !keep_rows || !unit_offsets) return ZS_ERR_ARG;
+  const int grid = grid_for_rows(U, 8);
+  keep_count_kernel<<<grid, 256, 0, S(stream)>>>(U, S_, K, is_pad, unit_offsets);
+  keep_scan_kernel<<<1, 1024, 0, S(stream)>>>(U, unit_offsets);
+  keep_write_kernel<<<grid, 256, 0, S(stream)>>>(U, S_, K, is_pad, unit_offsets, keep_rows);
+  return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
+}
+
+extern "C" int zs_patchify(const float* img, int B, int Cin, int H, int W, int P, void* out, zs_stream_t stream) {
+  if (B <= 0) return 0;
+  if (!img || !out || P <= 0 || H % P || W % P) return ZS_ERR_SHAPE;
+  patchify_kernel<<<num_sms() * 8, 256, 0, S(stream)>>>(img, B, Cin, H, W, P,
+                                                         reinterpret_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
+}
+
+extern "C" int zs_im2col3x3(const void* x, int B, int H, int W, int C, void* out, zs_stream_t stream) {
+  if (B <= 0) return 0;
+  if (!x || !out) return ZS_ERR_ARG;
+  im2col3x3_kernel<<<num_sms() * 8, 256, 0, S(stream)>>>(reinterpret_cast<const __nv_bfloat16*>(x), B, H, W, C,
+                                                          reinterpret_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
+}
