@@ -82,6 +82,10 @@ ZS_API int zs_permute_rows_f32(const float* src, float* dst, const int32_t* map,
                         zs_stream_t stream);
 ZS_API int zs_permute_rows_bf16(const void* src, void* dst, const int32_t* map, long long rows_out, int C,
                          zs_stream_t stream);
+/* Same gather, fp32 rows in, bf16 rows out (map may be NULL = identity): the cast
+ * that feeds a bf16 GEMM operand from the fp32 residual stream. */
+ZS_API int zs_permute_rows_f32_bf16(const float* src, void* dst, const int32_t* map, long long rows_out, int C,
+                             zs_stream_t stream);
 
 /* Row maps between the three token layouts of a batch of B images on an
  * H x W grid with `window` windows (nwin = ceil(H/window)*ceil(W/window)):
@@ -94,11 +98,12 @@ ZS_API int zs_permute_rows_bf16(const void* src, void* dst, const int32_t* map, 
  *   l_from_g [B*nwin*window^2]  G row feeding L row, -1 for pads
  *   s_from_g [B*H*W]            G row feeding S row
  *   s_from_l [B*H*W]            L row feeding S row
+ *   g_from_s [B*H*W]            S row feeding G row
  *   l_is_pad [B*nwin*window^2]  1 for pad rows of L
  * replaces: the per-block permute / inverse-permute in encoder.py:297-306, :343-368. */
 ZS_API int zs_layout_maps(const int32_t* sigma_glob, const int32_t* sigma_loc, int B, int H, int W, int window,
                    int32_t* l_from_s, int32_t* g_from_l, int32_t* l_from_g, int32_t* s_from_g, int32_t* s_from_l,
-                   uint8_t* l_is_pad, zs_stream_t stream);
+                   int32_t* g_from_s, uint8_t* l_is_pad, zs_stream_t stream);
 
 /* Prefix keep-set rows for RC-MLP routing in a σ-ordered layout: unit u owns
  * rows [u*S, (u+1)*S); its first K rows are kept unless is_pad (may be NULL) marks them.
@@ -108,6 +113,10 @@ ZS_API int zs_layout_maps(const int32_t* sigma_glob, const int32_t* sigma_loc, i
  * replaces: mlp.py:73-75,107 `keep_count` + `sigma.forward[:K]`. */
 ZS_API int zs_prefix_keep_rows(int U, int S, int K, const uint8_t* is_pad, int32_t* keep_rows, int32_t* unit_offsets,
                         zs_stream_t stream);
+/* Generalisation: rows [begin, end) of every unit, pads skipped (the bypass set is
+ * the span [K, S)).  rows holds U*(end-begin) entries. */
+ZS_API int zs_unit_span_rows(int U, int S, int begin, int end, const uint8_t* is_pad, int32_t* rows,
+                             int32_t* unit_offsets, zs_stream_t stream);
 
 /* ------------------------------------------------------------------ layernorm
  * out[i, :] = LN(x[rows ? rows[i] : i, :]) * gamma + beta  (population variance),
@@ -149,7 +158,8 @@ ZS_API int zs_stripe_attn_fwd(const void* q, const void* k, const void* v, long 
 /* ------------------------------------------------------------------- RC-MLP
  * Residual-consistency MLP on an fp32 residual stream x[rows, C] in place:
  *   kept rows  (keep_rows[0..n_keep)):  x += fc2(gelu(fc1(LN(x)) + b1)) + b2
- *   bypass rows (bypass_mode 1 only, bypass_rows[0..n_bypass)): x = LN(x)
+ *   bypass rows (bypass_mode 1 only, bypass_rows[0..n_bypass)): x = LN(x),
+ *               n_bypass = n_bypass_dev ? min(*n_bypass_dev, max_bypass) : max_bypass
  * n_keep = n_keep_dev ? min(*n_keep_dev, max_keep) : max_keep (device-side count,
  * so a data-dependent keep-set needs no host synchronisation).
  * w1 [hidden, C], w2 [C, hidden] bf16; workspace ws >= max_keep*(C+hidden) bf16.
@@ -157,7 +167,7 @@ ZS_API int zs_stripe_attn_fwd(const void* q, const void* k, const void* v, long 
 ZS_API int zs_rc_mlp_fwd(float* x, long long ldx, const int32_t* keep_rows, int max_keep, const int32_t* n_keep_dev,
                   int C, int hidden, const float* ln_g, const float* ln_b, float eps, const void* w1,
                   const float* b1, const void* w2, const float* b2, int bypass_mode, const int32_t* bypass_rows,
-                  int n_bypass, void* ws, zs_stream_t stream);
+                  int max_bypass, const int32_t* n_bypass_dev, void* ws, zs_stream_t stream);
 
 /* ------------------------------------------------------- SAM frame helpers
  * im2col for non-overlapping PxP patches of an fp32 NCHW image batch:

@@ -27,13 +27,15 @@ SIGNATURES: dict[str, list] = {
     "zs_rank_order": [_p, _i, _i, _i, _i, _i, _i, _i, _p, _p, _p, _p],
     "zs_permute_rows_f32": [_p, _p, _p, _ll, _i, _p],
     "zs_permute_rows_bf16": [_p, _p, _p, _ll, _i, _p],
-    "zs_layout_maps": [_p, _p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p],
+    "zs_permute_rows_f32_bf16": [_p, _p, _p, _ll, _i, _p],
+    "zs_layout_maps": [_p, _p, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _p, _p],
     "zs_prefix_keep_rows": [_i, _i, _i, _p, _p, _p, _p],
+    "zs_unit_span_rows": [_i, _i, _i, _i, _p, _p, _p, _p],
     "zs_layernorm_rows": [_p, _ll, _p, _ll, _i, _p, _p, _f, _p, _ll, _i, _p],
     "zs_gemm_bf16": [_i, _p, _ll, _p, _ll, _i, _i, _i, _p, _p, _ll, _p, _ll, _p, _p, _i, _p, _p],
     "zs_stripe_attn_fwd": [_p, _p, _p, _ll, _ll, _ll, _ll, _ll, _i, _i, _i, _i, _i, _p, _p, _i, _p, _p, _i, _i,
                            _i, _f, _p, _ll, _ll, _p],
-    "zs_rc_mlp_fwd": [_p, _ll, _p, _i, _p, _i, _i, _p, _p, _f, _p, _p, _p, _p, _i, _p, _i, _p, _p],
+    "zs_rc_mlp_fwd": [_p, _ll, _p, _i, _p, _i, _i, _p, _p, _f, _p, _p, _p, _p, _i, _p, _i, _p, _p, _p],
     "zs_patchify": [_p, _i, _i, _i, _i, _i, _p, _p],
     "zs_im2col3x3": [_p, _i, _i, _i, _i, _p, _p],
 }
@@ -70,7 +72,15 @@ def status_string(rc: int) -> str:
     return load().zs_status_string(rc).decode()
 
 
+# kernel launches issued per successful ABI call (composites launch several)
+LAUNCHES_PER_CALL = {"zs_rc_mlp_fwd": 3, "zs_unit_span_rows": 3, "zs_prefix_keep_rows": 3, "zs_layout_maps": 3,
+                     "zs_abi_version": 0}
+launch_count = 0
+
+
 def call(name: str, *args) -> None:
+    global launch_count
     rc = getattr(load(), name)(*args)
     if rc != 0:
         raise RuntimeError(f"{name} failed: zs_status {rc} ({status_string(rc)})")
+    launch_count += LAUNCHES_PER_CALL.get(name, 1)

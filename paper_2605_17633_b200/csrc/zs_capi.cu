@@ -99,8 +99,8 @@ extern "C" int zs_gemm_bf16(int epi, const void* A, long long lda, const void* W
 extern "C" int zs_rc_mlp_fwd(float* x, long long ldx, const int32_t* keep_rows, int max_keep,
                              const int32_t* n_keep_dev, int C, int hidden, const float* ln_g, const float* ln_b,
                              float eps, const void* w1, const float* b1, const void* w2, const float* b2,
-                             int bypass_mode, const int32_t* bypass_rows, int n_bypass, void* ws,
-                             zs_stream_t stream) {
+                             int bypass_mode, const int32_t* bypass_rows, int max_bypass,
+                             const int32_t* n_bypass_dev, void* ws, zs_stream_t stream) {
   if (!x || !keep_rows || !ln_g || !ln_b || !w1 || !w2 || !ws) return ZS_ERR_ARG;
   if (bypass_mode != 0 && bypass_mode != 1) return ZS_ERR_ARG;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -111,10 +111,11 @@ extern "C" int zs_rc_mlp_fwd(float* x, long long ldx, const int32_t* keep_rows, 
     rc = launch_layernorm(x, ldx, keep_rows, nullptr, max_keep, n_keep_dev, C, ln_g, ln_b, eps, hln, C, 0, st);
     if (rc) return rc;
   }
-  if (bypass_mode == 1 && n_bypass > 0) {
+  if (bypass_mode == 1 && max_bypass > 0) {
     if (!bypass_rows) return ZS_ERR_ARG;
     // x[bypass] = LN(x[bypass]) in place: per-row read-then-write, rows disjoint from keep_rows
-    rc = launch_layernorm(x, ldx, bypass_rows, bypass_rows, n_bypass, nullptr, C, ln_g, ln_b, eps, x, ldx, 1, st);
+    rc = launch_layernorm(x, ldx, bypass_rows, bypass_rows, max_bypass, n_bypass_dev, C, ln_g, ln_b, eps, x, ldx, 1,
+                          st);
     if (rc) return rc;
   }
   if (max_keep <= 0) return 0;

@@ -150,12 +150,35 @@ __global__ void maps_local_kernel(const int* __restrict__ sig_loc, int B, int H,
     }
   }
 }
-__global__ void maps_global_kernel(const int* __restrict__ sig_glob, int B, int HW, int* s_from_g) {
+__global__ void maps_global_kernel(const int* __restrict__ sig_glob, int B, int HW, int* s_from_g, int* g_from_s) {
   const long long total = (long long)B * HW;
   for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < total;
        g += (long long)gridDim.x * blockDim.x) {
     const int b = (int)(g / HW);
-    s_from_g[(long long)b * HW + sig_glob[g]] = (int)g;
+    const int s = b * HW + sig_glob[g];
+    if (s_from_g) s_from_g[s] = (int)g;
+    if (g_from_s) g_from_s[g] = s;
+  }
+}
+
+// fp32 rows -> bf16 rows through a row map (pads / negative map -> zeros)
+__global__ void __launch_bounds__(256) permute_f32_bf16_kernel(const float4* __restrict__ src,
+                                                               uint2* __restrict__ dst,
+                                                               const int* __restrict__ map, long long rows,
+                                                               int nvec) {
+  const int lane = threadIdx.x & 31;
+  for (long long r = (long long)blockIdx.x * 8 + (threadIdx.x >> 5); r < rows; r += (long long)gridDim.x * 8) {
+    const int s = map ? map[r] : (int)r;
+    uint2* d = dst + r * nvec;
+    for (int c = lane; c < nvec; c += 32) {
+      uint2 w = make_uint2(0u, 0u);
+      if (s >= 0) {
+        const float4 v = src[(long long)s * nvec + c];
+        w.x = pack_bf16(v.x, v.y);
+        w.y = pack_bf16(v.z, v.w);
+      }
+      d[c] = w;
+    }
   }
 }
 __global__ void maps_cross_kernel(const int* __restrict__ sig_glob, int B, int HW, long long nl,
@@ -177,12 +200,13 @@ __global__ void maps_cross_kernel(const int* __restrict__ sig_glob, int B, int H
 }
 
 // ------------------------------------------------------------------ keep rows
-// counts[u] = # non-pad rows among the first K rows of unit u
-__global__ void keep_count_kernel(int U, int S, int K, const unsigned char* __restrict__ is_pad, int* counts) {
+// counts[u] = # non-pad rows among rows [k0, k1) of unit u
+__global__ void keep_count_kernel(int U, int S, int k0, int k1, const unsigned char* __restrict__ is_pad,
+                                  int* counts) {
   const int lane = threadIdx.x & 31;
   for (int u = blockIdx.x * 8 + (threadIdx.x >> 5); u < U; u += gridDim.x * 8) {
     int c = 0;
-    for (int i = lane; i < K; i += 32) c += is_pad ? (is_pad[(long long)u * S + i] == 0) : 1;
+    for (int i = k0 + lane; i < k1; i += 32) c += is_pad ? (is_pad[(long long)u * S + i] == 0) : 1;
 #pragma unroll
     for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
     if (lane == 0) counts[u] = c;
@@ -224,15 +248,15 @@ __global__ void __launch_bounds__(1024) keep_scan_kernel(int U, int* counts) {
   }
   if (threadIdx.x == 0) counts[U] = carry;
 }
-__global__ void keep_write_kernel(int U, int S, int K, const unsigned char* __restrict__ is_pad,
+__global__ void keep_write_kernel(int U, int S, int k0, int k1, const unsigned char* __restrict__ is_pad,
                                   const int* __restrict__ offsets, int* keep_rows) {
   const int lane = threadIdx.x & 31;
   for (int u = blockIdx.x * 8 + (threadIdx.x >> 5); u < U; u += gridDim.x * 8) {
     int pos = offsets[u];
-    for (int i0 = 0; i0 < K; i0 += 32) {
+    for (int i0 = k0; i0 < k1; i0 += 32) {
       const int i = i0 + lane;
       const long long r = (long long)u * S + i;
-      const bool keep = i < K && (!is_pad || is_pad[r] == 0);
+      const bool keep = i < k1 && (!is_pad || is_pad[r] == 0);
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (keep) keep_rows[pos + __popc(m & ((1u << lane) - 1u))] = (int)r;
       pos += __popc(m);
@@ -310,9 +334,20 @@ extern "C" int zs_permute_rows_bf16(const void* src, void* dst, const int32_t* m
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }
 
+extern "C" int zs_permute_rows_f32_bf16(const float* src, void* dst, const int32_t* map, long long rows_out, int C,
+                                        zs_stream_t stream) {
+  if (rows_out <= 0) return 0;
+  if (!src || !dst) return ZS_ERR_ARG;
+  if (C <= 0 || C % 4) return ZS_ERR_SHAPE;
+  if ((reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 7)) return ZS_ERR_ALIGN;
+  permute_f32_bf16_kernel<<<grid_for_rows(rows_out, 8), 256, 0, S(stream)>>>(
+      reinterpret_cast<const float4*>(src), reinterpret_cast<uint2*>(dst), map, rows_out, C / 4);
+  return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
+}
+
 extern "C" int zs_layout_maps(const int32_t* sigma_glob, const int32_t* sigma_loc, int B, int H, int W, int window,
                               int32_t* l_from_s, int32_t* g_from_l, int32_t* l_from_g, int32_t* s_from_g,
-                              int32_t* s_from_l, uint8_t* l_is_pad, zs_stream_t stream) {
+                              int32_t* s_from_l, int32_t* g_from_s, uint8_t* l_is_pad, zs_stream_t stream) {
   if (B <= 0 || H <= 0 || W <= 0 || window <= 0) return ZS_ERR_SHAPE;
   const int nwy = (H + window - 1) / window, nwx = (W + window - 1) / window;
   const int nwin = nwy * nwx;
@@ -323,24 +358,31 @@ extern "C" int zs_layout_maps(const int32_t* sigma_glob, const int32_t* sigma_lo
     return ZS_ERR_ARG;
   if (sigma_loc) maps_local_kernel<<<grid, 256, 0, S(stream)>>>(sigma_loc, B, H, W, window, nwx, nwin, l_from_s,
                                                                  s_from_l, l_is_pad);
-  if (sigma_glob && s_from_g) maps_global_kernel<<<grid, 256, 0, S(stream)>>>(sigma_glob, B, HW, s_from_g);
+  if (sigma_glob && (s_from_g || g_from_s))
+    maps_global_kernel<<<grid, 256, 0, S(stream)>>>(sigma_glob, B, HW, s_from_g, g_from_s);
   if (g_from_l || l_from_g)
     maps_cross_kernel<<<grid, 256, 0, S(stream)>>>(sigma_glob, B, HW, nl, s_from_l, s_from_g, l_from_s, g_from_l,
                                                     l_from_g);
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }
 
-// keep_rows must hold U*K entries; unit_offsets must hold U+1 entries and
-// receives the exclusive prefix of per-unit kept counts (total at [U]).
+// rows must hold U*(k1-k0) entries; unit_offsets must hold U+1 entries and
+// receives the exclusive prefix of per-unit selected counts (total at [U]).
+extern "C" int zs_unit_span_rows(int U, int S_, int k0, int k1, const uint8_t* is_pad, int32_t* rows,
+                                 int32_t* unit_offsets, zs_stream_t stream) {
+  if (U <= 0) return 0;
+  if (k0 < 0 || k1 < k0 || k1 > S_ || !rows || !unit_offsets) return ZS_ERR_ARG;
+  const int grid = grid_for_rows(U, 8);
+  keep_count_kernel<<<grid, 256, 0, S(stream)>>>(U, S_, k0, k1, is_pad, unit_offsets);
+  keep_scan_kernel<<<1, 1024, 0, S(stream)>>>(U, unit_offsets);
+  keep_write_kernel<<<grid, 256, 0, S(stream)>>>(U, S_, k0, k1, is_pad, unit_offsets, rows);
+  return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
+}
+
 extern "C" int zs_prefix_keep_rows(int U, int S_, int K, const uint8_t* is_pad, int32_t* keep_rows,
                                    int32_t* unit_offsets, zs_stream_t stream) {
-  if (U <= 0) return 0;
-  if (K <= 0 || K > S_ || !keep_rows || !unit_offsets) return ZS_ERR_ARG;
-  const int grid = grid_for_rows(U, 8);
-  keep_count_kernel<<<grid, 256, 0, S(stream)>>>(U, S_, K, is_pad, unit_offsets);
-  keep_scan_kernel<<<1, 1024, 0, S(stream)>>>(U, unit_offsets);
-  keep_write_kernel<<<grid, 256, 0, S(stream)>>>(U, S_, K, is_pad, unit_offsets, keep_rows);
-  return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
+  if (K <= 0) return ZS_ERR_ARG;
+  return zs_unit_span_rows(U, S_, 0, K, is_pad, keep_rows, unit_offsets, stream);
 }
 
 extern "C" int zs_patchify(const float* img, int B, int Cin, int H, int W, int P, void* out, zs_stream_t stream) {

@@ -1,0 +1,309 @@
+"""SparseSAM encoder on B200: the block loop of encoder.py:310-385 over device layouts.
+
+Token layouts (rows of the fp32 residual stream, C columns):
+  S  spatial   b*HW + y*W + x                       (input / output order)
+  L  local     (b*nwin + w)*win^2 + i  = token sigma_w[b,w,i] of window w,
+               pad tokens of the zero-padded grid included (kept at zero)
+  G  global    b*HW + i                = token sigma_g[b,i]
+
+Because LayerNorm, the projections and the MLP are row-wise, every block runs
+directly in its scan-ordered layout: attention sees sigma-ordered Q/K/V rows
+without any per-head gather, the RC-MLP keep-set is the first K rows of each
+unit, and the residual stream only moves when consecutive blocks change kind
+(one ``zs_permute_rows_f32`` per switch).  Local pads are re-zeroed by the
+projection epilogue, which is exactly the reference's re-padding at every
+local block (encoder.py:356); their MLP rows are skipped (output-exact, since
+the crop discards them, encoder.py:366-368).
+
+The orderings come once per image from the fp32 block-0 input
+(encoder.py:334): Sobel saliency, z-group energy, stable rank,
+stripe interleave — all on device, bit-exact with the reference.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import kernels as K
+from .config import SAM_NECK, SAM_PATCH, EncoderConfig, RouterConfig
+from .trace import NULL
+from .weights import BlockParams, FrameParams
+
+
+def attention_elements(S: int, tile: int, prefix: int) -> int:
+    """E = sum_i sum_{j in J_i} |rows_i| * |cols_j|: score elements the static schedule requires."""
+    T = -(-S // tile)
+
+    def size(t):
+        return min((t + 1) * tile, S) - t * tile
+
+    total = 0
+    for i in range(T):
+        cols = set(range(min(prefix, T))) | {min(i, T - 1)}
+        total += size(i) * sum(size(j) for j in cols)
+    return total
+
+
+def morton_order_np(h: int, w: int) -> np.ndarray:
+    """Token index at each Morton rank (x bits even, y bits odd; grid.py:79-104).
+
+    Host-side constant table built once per grid shape."""
+    ys, xs = np.divmod(np.arange(h * w, dtype=np.uint64), np.uint64(w))
+
+    def spread(v):
+        v = v & np.uint64(0xFFFFFFFF)
+        for s, m in ((16, 0x0000FFFF0000FFFF), (8, 0x00FF00FF00FF00FF), (4, 0x0F0F0F0F0F0F0F0F),
+                     (2, 0x3333333333333333), (1, 0x5555555555555555)):
+            v = (v | (v << np.uint64(s))) & np.uint64(m)
+        return v
+
+    codes = spread(xs) | (spread(ys) << np.uint64(1))
+    return np.argsort(codes, kind="stable").astype(np.int64)
+
+
+@dataclass
+class Orderings:
+    sigma_glob: torch.Tensor | None  # [B, HW] int32
+    sigma_loc: torch.Tensor | None  # [B*nwin, win^2] int32
+    maps: dict
+
+
+class StripeSortEncoder:
+    """Runs the SparseSAM block stack on a batch of fp32 token grids ``[B, H, W, C]``.
+
+    ``mode="sparse"`` uses the per-block r / keep_fraction of ``cfg``;
+    ``mode="dense"`` pins r = keep = 1 through the same kernels (the reference's
+    dense twin, encoder.py:338-339).
+    """
+
+    def __init__(self, cfg: EncoderConfig, params: list[BlockParams], device="cuda"):
+        if len(params) != len(cfg.layout):
+            raise ValueError(f"{len(params)} weight sets for {len(cfg.layout)} blocks")
+        hd = cfg.head_dim
+        if hd not in (64, 80):
+            raise ValueError(f"head dim {hd} unsupported by the B200 attention kernel (64 or 80)")
+        if cfg.d % 64:
+            raise ValueError("model width must be a multiple of 64 for the tcgen05 GEMMs")
+        self.cfg = cfg
+        self.params = params
+        self.device = torch.device(device)
+        g = cfg.grid
+        self.HW = g.n()
+        self.win = cfg.window
+        self.S2 = cfg.window**2
+        self.nwin = cfg.nwin()
+        i32 = dict(device=self.device, dtype=torch.int32)
+        self.morton_g = torch.as_tensor(morton_order_np(g.h, g.w)).to(**i32)
+        self.morton_w = torch.as_tensor(morton_order_np(cfg.window, cfg.window)).to(**i32)
+        self._ws: dict = {}
+        self._ws_B = None
+        self.has_local = "local" in cfg.layout
+        self.has_global = "global" in cfg.layout
+        self.tracer = NULL
+
+    # ------------------------------------------------------------ workspace
+    def _workspace(self, B: int) -> dict:
+        if self._ws_B == B:
+            return self._ws
+        C = self.cfg.d
+        dev = self.device
+        RL = B * self.nwin * self.S2 if self.has_local else 0
+        RG = B * self.HW
+        R = max(RL, RG)
+        ws = dict(
+            xa=torch.empty((R, C), device=dev, dtype=torch.float32),
+            xb=torch.empty((R, C), device=dev, dtype=torch.float32),
+            h=torch.empty((R, C), device=dev, dtype=torch.bfloat16),
+            qkv=torch.empty((R, 3 * C), device=dev, dtype=torch.bfloat16),
+            o=torch.empty((R, C), device=dev, dtype=torch.bfloat16),
+            mlp=torch.empty((0,), device=dev, dtype=torch.bfloat16),
+        )
+        self._ws, self._ws_B = ws, B
+        return ws
+
+    # ------------------------------------------------------------ ordering
+    def orderings(self, x0: torch.Tensor) -> Orderings:
+        """sigma_global / sigma_local from the fp32 block-0 input ``x0[B,H,W,C]`` (encoder.py:257-275)."""
+        cfg = self.cfg
+        B = x0.shape[0]
+        sg, sw = K.sobel_saliency(x0, self.win, glob=self.has_global, win=self.has_local)
+        kw = dict(granularity=cfg.ordering.granularity, group_size=cfg.ordering.group_size, g=cfg.stripe.g,
+                  variant=cfg.stripe.variant)
+        sig_g = K.rank_order(sg.reshape(B, self.HW), self.morton_g, **kw)[0] if self.has_global else None
+        sig_l = K.rank_order(sw.reshape(B * self.nwin, self.S2), self.morton_w, **kw)[0] if self.has_local else None
+        maps = K.layout_maps(sig_g, sig_l, B, cfg.grid.h, cfg.grid.w, self.win)
+        return Orderings(sig_g, sig_l, maps)
+
+    def _row_sets(self, B: int, od: Orderings, mode: str) -> dict:
+        """Keep-set (σ prefix) and bypass rows per distinct (kind, K), device-side counts."""
+        cfg = self.cfg
+        sets = {}
+        for bi, kind in enumerate(cfg.layout):
+            kf = 1.0 if mode == "dense" else cfg.keep_fraction[bi]
+            S = self.S2 if kind == "local" else self.HW
+            U = B * self.nwin if kind == "local" else B
+            Kc = RouterConfig(kf, cfg.bypass_mode).keep_count(S)
+            key = (kind, Kc)
+            if key in sets:
+                continue
+            pad = od.maps.get("l_is_pad") if kind == "local" else None
+            keep, koff = K.unit_span_rows(U, S, 0, Kc, pad, self.device)
+            entry = dict(keep=keep, n_keep=koff[U:U + 1], max_keep=U * Kc)
+            if cfg.bypass_mode == "layernorm" and Kc < S:
+                byp, boff = K.unit_span_rows(U, S, Kc, S, pad, self.device)
+                entry.update(bypass=byp, n_bypass=boff[U:U + 1])
+            sets[key] = entry
+        need = max(e["max_keep"] for e in sets.values()) * 5 * cfg.d
+        ws = self._ws
+        if ws["mlp"].numel() < need:
+            ws["mlp"] = torch.empty((need,), device=self.device, dtype=torch.bfloat16)
+        return sets
+
+    # ------------------------------------------------------------ blocks
+    def _block(self, blk: BlockParams, x: torch.Tensor, od: Orderings, B: int, r: float, rows: dict,
+               ws: dict) -> None:
+        cfg = self.cfg
+        C, H, dh = cfg.d, cfg.heads, cfg.head_dim
+        local = blk.kind == "local"
+        S = self.S2 if local else self.HW
+        U = B * self.nwin if local else B
+        R = U * S
+        tile = cfg.tile(blk.kind)
+        T = -(-S // tile)
+        prefix = math.floor(r * T)
+        sig = od.sigma_loc if local else od.sigma_glob
+        xs = x[:R]
+        tr = self.tracer
+        w = blk.bh.shape[-1]
+        with tr.span("layernorm", bytes=R * C * 6):
+            h = K.layernorm_rows(xs, blk.ln1_g, blk.ln1_b, out=ws["h"][:R])
+        with tr.span("gemm", flops=2.0 * R * C * 3 * C, bytes=R * C * 2 + 3 * C * C * 2 + R * 3 * C * 2):
+            qkv = K.gemm(h, blk.qkv_w, blk.qkv_b, out=ws["qkv"][:R])
+        E = attention_elements(S, tile, prefix)
+        with tr.span(f"attn_{blk.kind}", flops=4.0 * dh * E * U * H,
+                     bytes=U * H * 4 * S * dh * 2 + H * 2 * S * w * 4):
+            o = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], units=U, heads=H, sq=S, sk=S, dh=dh,
+                              bh=blk.bh, bw=blk.bw, q_sp=sig, k_sp=sig, b_row=tile, b_col=tile, prefix=prefix,
+                              tau=1.0 / math.sqrt(dh), out=ws["o"][:R])
+        with tr.span("gemm", flops=2.0 * R * C * C, bytes=R * C * 2 + C * C * 2 + R * C * 8):
+            K.gemm(o, blk.proj_w, blk.proj_b, epi=K.EPI_F32_RESID, out=xs, res=xs,
+                   zero_rows=od.maps["l_is_pad"] if local else None)
+        nk = rows["n_keep"]
+        with tr.span("rc_mlp", flops=(nk, 16.0 * C * C), bytes=(nk, C * 4 * 2 + C * 2 + 8 * C * 2)):
+            K.rc_mlp(xs, rows["keep"], n_keep_dev=nk, ln_g=blk.ln2_g, ln_b=blk.ln2_b, w1=blk.w1, b1=blk.b1,
+                     w2=blk.w2, b2=blk.b2, bypass_rows=rows.get("bypass"), n_bypass_dev=rows.get("n_bypass"),
+                     ws=ws["mlp"])
+
+    def forward_rows(self, x0: torch.Tensor, mode: str = "sparse", orderings: Orderings | None = None,
+                     out: torch.Tensor | None = None) -> torch.Tensor:
+        """fp32 ``x0[B,H,W,C]`` -> fp32 ``[B*H*W, C]`` spatial rows after every block."""
+        if mode not in ("dense", "sparse"):
+            raise ValueError(f"mode must be 'dense' or 'sparse', got {mode!r}")
+        cfg = self.cfg
+        if x0.dim() != 4 or tuple(x0.shape[1:]) != (cfg.grid.h, cfg.grid.w, cfg.d):
+            raise ValueError(f"input shape {tuple(x0.shape)} != (B, {cfg.grid.h}, {cfg.grid.w}, {cfg.d})")
+        if x0.dtype != torch.float32 or not x0.is_cuda:
+            raise ValueError("x0 must be a float32 CUDA tensor")
+        x0 = x0.contiguous()
+        B = x0.shape[0]
+        ws = self._workspace(B)
+        if orderings is None:
+            with self.tracer.span("ordering", bytes=x0.numel() * 4):
+                orderings = self.orderings(x0)
+        od = orderings
+        rows = self._row_sets(B, od, mode)
+        m = od.maps
+        flat = x0.reshape(B * self.HW, cfg.d)
+        cur, spare = ws["xa"], ws["xb"]
+        layout = None
+        for bi, blk in enumerate(self.params):
+            kind = blk.kind
+            if kind != layout:
+                if layout is None:
+                    src, mp = flat, (m["l_from_s"] if kind == "local" else m["g_from_s"])
+                else:
+                    src, mp = cur, (m["l_from_g"] if kind == "local" else m["g_from_l"])
+                with self.tracer.span("permute", bytes=mp.numel() * cfg.d * 8):
+                    K.permute_rows(src, mp, out=spare[: mp.numel()])
+                cur, spare = spare, cur
+                layout = kind
+            r = 1.0 if mode == "dense" else cfg.r[bi]
+            kf = 1.0 if mode == "dense" else cfg.keep_fraction[bi]
+            S = self.S2 if kind == "local" else self.HW
+            Kc = RouterConfig(kf, cfg.bypass_mode).keep_count(S)
+            self._block(blk, cur, od, B, r, rows[(kind, Kc)], ws)
+        if out is None:
+            out = torch.empty((B * self.HW, cfg.d), device=self.device, dtype=torch.float32)
+        with self.tracer.span("permute", bytes=out.numel() * 8):
+            K.permute_rows(cur, m["s_from_l"] if layout == "local" else m["s_from_g"], out=out)
+        return out
+
+    def __call__(self, x0: torch.Tensor, mode: str = "sparse") -> torch.Tensor:
+        B = x0.shape[0]
+        return self.forward_rows(x0, mode).reshape(B, self.cfg.grid.h, self.cfg.grid.w, self.cfg.d)
+
+
+class SparseSAMImageEncoder:
+    """SAM ViT image encoder with SparseSAM blocks: 1024² image -> [B, 256, 64, 64].
+
+    patch embed (16x16/16 conv as patchify + tcgen05 GEMM, bias and absolute
+    position embedding fused in the epilogue) -> fp32 block-0 input (source of
+    the orderings) -> SparseSAM blocks -> neck (1x1 conv GEMM, LN2d, 3x3 conv
+    as im2col + GEMM, LN2d).  The frame is SAM's [ext]; parity for it is
+    pinned by an fp32 torch twin (tests), the blocks by the reference oracle.
+    """
+
+    def __init__(self, cfg: EncoderConfig, params: list[BlockParams], frame: FrameParams, device="cuda"):
+        self.cfg = cfg
+        self.frame = frame
+        self.core = StripeSortEncoder(cfg, params, device)
+        self.device = self.core.device
+        self._buf_B = None
+
+    def _bufs(self, B: int) -> dict:
+        if self._buf_B != B:
+            C, HW, dev = self.cfg.d, self.cfg.grid.n(), self.device
+            self._bufs_d = dict(
+                x0=torch.empty((B * HW, C), device=dev, dtype=torch.float32),
+                xo=torch.empty((B * HW, C), device=dev, dtype=torch.float32),
+                xb16=torch.empty((B * HW, C), device=dev, dtype=torch.bfloat16),
+                n1=torch.empty((B * HW, SAM_NECK), device=dev, dtype=torch.float32),
+                n1b=torch.empty((B * HW, SAM_NECK), device=dev, dtype=torch.bfloat16),
+                n2=torch.empty((B * HW, SAM_NECK), device=dev, dtype=torch.float32),
+                out=torch.empty((B * HW, SAM_NECK), device=dev, dtype=torch.float32),
+            )
+            self._buf_B = B
+        return self._bufs_d
+
+    def embed(self, img: torch.Tensor) -> torch.Tensor:
+        """fp32 NCHW image -> fp32 token grid rows [B*HW, C] (patch embed + pos)."""
+        B = img.shape[0]
+        bufs = self._bufs(B)
+        patches = K.patchify(img, SAM_PATCH)
+        f = self.frame
+        K.gemm(patches, f.pe_w, f.pe_b, epi=K.EPI_F32_RESID, out=bufs["x0"], res=f.pos, res_mod=self.cfg.grid.n())
+        return bufs["x0"]
+
+    def neck(self, rows: torch.Tensor, B: int) -> torch.Tensor:
+        f = self.frame
+        bufs = self._bufs(B)
+        g = self.cfg.grid
+        xb = K.cast_rows_bf16(rows, out=bufs["xb16"])
+        K.gemm(xb, f.neck1_w, None, epi=K.EPI_F32_RESID, out=bufs["n1"])
+        K.layernorm_rows(bufs["n1"], f.neck_ln1_g, f.neck_ln1_b, out=bufs["n1b"])
+        cols = K.im2col3x3(bufs["n1b"].view(B, g.h, g.w, SAM_NECK))
+        K.gemm(cols, f.neck2_w, None, epi=K.EPI_F32_RESID, out=bufs["n2"])
+        K.layernorm_rows(bufs["n2"], f.neck_ln2_g, f.neck_ln2_b, out_f32=True, out=bufs["out"])
+        return bufs["out"].view(B, g.h, g.w, SAM_NECK)
+
+    def __call__(self, img: torch.Tensor, mode: str = "sparse") -> torch.Tensor:
+        """[B, 3, 1024, 1024] fp32 -> channels-last embeddings [B, 64, 64, 256] fp32."""
+        B = img.shape[0]
+        g = self.cfg.grid
+        x0 = self.embed(img)
+        xo = self.core.forward_rows(x0.view(B, g.h, g.w, self.cfg.d), mode, out=self._bufs(B)["xo"])
+        return self.neck(xo, B)

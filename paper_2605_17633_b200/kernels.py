@@ -128,6 +128,17 @@ def permute_rows(src: torch.Tensor, row_map: torch.Tensor, out: torch.Tensor | N
     return out
 
 
+def cast_rows_bf16(src: torch.Tensor, row_map: torch.Tensor | None = None,
+                   out: torch.Tensor | None = None) -> torch.Tensor:
+    """bf16 copy of fp32 rows, optionally gathered through ``row_map``."""
+    _need(src, torch.float32, "src")
+    rows = src.shape[0] if row_map is None else row_map.numel()
+    if out is None:
+        out = torch.empty((rows, src.shape[1]), device=src.device, dtype=torch.bfloat16)
+    _lib.call("zs_permute_rows_f32_bf16", _ptr(src), _ptr(out), _ptr(row_map), rows, src.shape[1], _stream())
+    return out
+
+
 # ------------------------------------------------------------------ ordering
 def sobel_saliency(x: torch.Tensor, window: int, *, glob: bool = True, win: bool = True):
     """fp32 ``x[B,H,W,C]`` -> (``sal_glob[B,H,W]`` | None, ``sal_win[B,nwin,window^2]`` | None)."""
@@ -185,22 +196,28 @@ def layout_maps(sigma_glob: torch.Tensor | None, sigma_loc: torch.Tensor | None,
         m["l_is_pad"] = torch.empty(nl, device=dev, dtype=torch.uint8)
     if sigma_glob is not None:
         m["s_from_g"] = torch.empty(ng, **i32)
+        m["g_from_s"] = torch.empty(ng, **i32)
     if sigma_glob is not None and sigma_loc is not None:
         m["g_from_l"] = torch.empty(ng, **i32)
         m["l_from_g"] = torch.empty(nl, **i32)
     _lib.call("zs_layout_maps", _ptr(sigma_glob), _ptr(sigma_loc), B, H, W, window, _ptr(m.get("l_from_s")),
               _ptr(m.get("g_from_l")), _ptr(m.get("l_from_g")), _ptr(m.get("s_from_g")), _ptr(m.get("s_from_l")),
-              _ptr(m.get("l_is_pad")), _stream())
+              _ptr(m.get("g_from_s")), _ptr(m.get("l_is_pad")), _stream())
     return m
+
+
+def unit_span_rows(U: int, S: int, begin: int, end: int, is_pad: torch.Tensor | None, device=None):
+    """Rows [begin, end) of every S-row unit (pads skipped) and per-unit offsets (total at [U])."""
+    dev = is_pad.device if is_pad is not None else device
+    rows = torch.empty(max(U * (end - begin), 1), device=dev, dtype=torch.int32)
+    offs = torch.empty(U + 1, device=dev, dtype=torch.int32)
+    _lib.call("zs_unit_span_rows", U, S, begin, end, _ptr(is_pad), _ptr(rows), _ptr(offs), _stream())
+    return rows[: U * (end - begin)], offs
 
 
 def prefix_keep_rows(U: int, S: int, K: int, is_pad: torch.Tensor | None, device=None):
     """Kept rows (first K of every S-row unit, pads skipped) and per-unit offsets (total at [U])."""
-    dev = is_pad.device if is_pad is not None else device
-    keep = torch.empty(U * K, device=dev, dtype=torch.int32)
-    offs = torch.empty(U + 1, device=dev, dtype=torch.int32)
-    _lib.call("zs_prefix_keep_rows", U, S, K, _ptr(is_pad), _ptr(keep), _ptr(offs), _stream())
-    return keep, offs
+    return unit_span_rows(U, S, 0, K, is_pad, device)
 
 
 # ------------------------------------------------------------------ attention
@@ -263,6 +280,7 @@ def rc_mlp(
     b2: torch.Tensor,
     n_keep_dev: torch.Tensor | None = None,
     bypass_rows: torch.Tensor | None = None,
+    n_bypass_dev: torch.Tensor | None = None,
     ws: torch.Tensor | None = None,
     eps: float = 1e-6,
 ) -> torch.Tensor:
@@ -278,7 +296,7 @@ def rc_mlp(
     nb = 0 if bypass_rows is None else bypass_rows.numel()
     _lib.call("zs_rc_mlp_fwd", _ptr(x), x.stride(0), _ptr(keep_rows), max_keep, _ptr(n_keep_dev), C, hidden,
               _ptr(ln_g), _ptr(ln_b), eps, _ptr(w1), _ptr(b1), _ptr(w2), _ptr(b2), 1 if bypass_rows is not None else 0,
-              _ptr(bypass_rows), nb, _ptr(ws), _stream())
+              _ptr(bypass_rows), nb, _ptr(n_bypass_dev), _ptr(ws), _stream())
     return x
 
 

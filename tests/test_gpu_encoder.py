@@ -1,0 +1,132 @@
+"""Encoder parity on the B200: blocks and full stacks vs the reference / oracle (marker: gpu).
+
+Tolerance (stated once, used everywhere below, BASELINE north star):
+  flat cosine similarity >= 0.999, relative Frobenius error <= 3e-2,
+  per-token minimum cosine >= 0.99, with the orderings bit-exact (they are
+  built from the fp32 input, so bf16 arithmetic never perturbs them).
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import zs_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_2605_17633_b200 as Z
+    from paper_2605_17633_b200 import api
+    from paper_2605_17633_b200.encoder import SparseSAMImageEncoder, StripeSortEncoder
+    from paper_2605_17633_b200.weights import params_from_reference, random_frame, random_params
+
+
+def assert_close(got, ref, what=""):
+    got = np.asarray(got, np.float64).reshape(-1, np.shape(ref)[-1])
+    ref = np.asarray(ref, np.float64).reshape(got.shape)
+    cos = float((got * ref).sum() / (np.linalg.norm(got) * np.linalg.norm(ref)))
+    relf = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+    tok = (got * ref).sum(1) / (np.linalg.norm(got, axis=1) * np.linalg.norm(ref, axis=1) + 1e-30)
+    assert cos >= 0.999 and relf <= 3e-2 and tok.min() >= 0.99, (what, cos, relf, tok.min())
+    return cos, relf, tok.min()
+
+
+def _oracle_to_ref_cfg(ocfg):
+    return Z.EncoderConfig(grid=Z.GridShape(ocfg.h, ocfg.w), d=ocfg.d, heads=ocfg.heads, window=ocfg.window,
+                           layout=ocfg.layout, r=ocfg.r, keep_fraction=ocfg.keep, seed=ocfg.seed)
+
+
+@pytest.mark.parametrize("mode", ["sparse", "dense"])
+def test_encoder_small_vs_reference(mode):
+    """4-block encoder (local, global, local, local) on a 20x20 grid with window 6 (pads)."""
+    g = golden("encoder_small")
+    ocfg = O.EncCfg(h=20, w=20, d=128, heads=2, window=6, layout=("local", "global", "local", "local"),
+                    r=(0.4,) * 4, keep=(0.4,) * 4, seed=5)
+    x = O.SplitMix(3).normal((20, 20, 128))
+    y, rep = api.encoder_forward(x, O.init_weights(ocfg), _oracle_to_ref_cfg(ocfg), mode=mode)
+    assert_close(y, g[mode], mode)
+
+
+def test_sparse_equals_dense_at_full_density_bitexact():
+    """mode='dense' is the same pipeline at r = keep = 1 (encoder.py:338-339): bit-identical on device."""
+    ocfg = O.EncCfg(h=20, w=20, d=128, heads=2, window=6, layout=("local", "global"), r=(1.0, 1.0),
+                    keep=(1.0, 1.0), seed=2)
+    cfg = _oracle_to_ref_cfg(ocfg)
+    params = params_from_reference(O.init_weights(ocfg), cfg, "cuda")
+    x = torch.from_numpy(O.SplitMix(4).normal((2, 20, 20, 128))).cuda()
+    enc = StripeSortEncoder(cfg, params)
+    assert torch.equal(enc(x, "sparse"), enc(x, "dense"))
+
+
+@pytest.mark.parametrize("kind", ["local", "global"])
+def test_config1_block_vs_reference(kind):
+    """Config 1: one SparseSAM ViT-B block (64x64, 768, 12 heads, density 0.4) vs the reference's output."""
+    g = golden("config1_blocks")
+    ocfg = O.EncCfg(layout=(kind,), r=(0.4,), keep=(0.4,))
+    x = O.SplitMix(1).normal((64, 64, 768))
+    y, _ = api.encoder_forward(x, O.init_weights(ocfg), _oracle_to_ref_cfg(ocfg))
+    flat = y.reshape(4096, 768)
+    assert_close(flat[g["rows"]], g[f"{kind}_rows"], kind)
+    np.testing.assert_allclose(flat.sum(1), g[f"{kind}_rowsum"], rtol=0, atol=0.35)
+
+
+def test_batched_images_are_independent():
+    """Batch of 3 == three single-image runs (orderings, layouts and keep-sets are per image)."""
+    ocfg = O.EncCfg(h=20, w=20, d=128, heads=2, window=6, layout=("local", "global", "local"), r=(0.4,) * 3,
+                    keep=(0.4,) * 3, seed=8)
+    cfg = _oracle_to_ref_cfg(ocfg)
+    enc = StripeSortEncoder(cfg, params_from_reference(O.init_weights(ocfg), cfg, "cuda"))
+    xs = torch.from_numpy(O.SplitMix(11).normal((3, 20, 20, 128))).cuda()
+    yb = enc(xs)
+    for i in range(3):
+        assert torch.equal(yb[i], enc(xs[i:i + 1])[0])
+
+
+def test_vit_b_full_encoder_vs_oracle():
+    """Config 2 parity path: the 12-block ViT-B layout (globals at 2/5/8/11) on Rng(1) tokens vs the oracle."""
+    cfg = Z.sam_config("vit_b", 0.4)
+    ocfg = O.EncCfg(layout=cfg.layout, r=cfg.r, keep=cfg.keep_fraction)
+    x = O.SplitMix(1).normal((64, 64, 768))
+    w = O.init_weights(ocfg)
+    ref = O.encoder_forward(x, w, ocfg)
+    y, rep = api.encoder_forward(x, w, cfg)
+    assert_close(y, ref, "vit_b")
+    assert rep.attn_density() < 0.5
+
+
+@pytest.mark.parametrize("model", ["vit_l", "vit_h"])
+def test_local_and_global_block_shapes_vs_oracle(model):
+    """ViT-L / ViT-H block geometry (C=1024/1280, 16 heads, dh 64/80) — block-level parity."""
+    base = Z.sam_config(model, 0.4)
+    ocfg = O.EncCfg(d=base.d, heads=base.heads, layout=("local", "global"), r=(0.4, 0.4), keep=(0.4, 0.4))
+    x = O.SplitMix(2).normal((64, 64, base.d))
+    w = O.init_weights(ocfg)
+    ref = O.encoder_forward(x, w, ocfg)
+    y, _ = api.encoder_forward(x, w, _oracle_to_ref_cfg(ocfg))
+    assert_close(y, ref, model)
+
+
+def test_sam_frame_vs_fp32_torch_twin():
+    """Patch embed + pos, neck (1x1 conv, LN2d, 3x3 conv, LN2d): builder-written fp32 twin (parity unpinned
+    by the reference); the blocks are bypassed by comparing embed and neck separately."""
+    cfg = Z.sam_config("vit_b", 0.4)
+    frame = random_frame(cfg, "cuda", seed=3)
+    enc = SparseSAMImageEncoder(cfg, random_params(cfg, "cuda", seed=1), frame)
+    img = torch.randn(2, 3, 1024, 1024, device="cuda")
+    x0 = enc.embed(img).clone()
+    wpe = frame.pe_w.float().view(cfg.d, 3, 16, 16)
+    ref = torch.nn.functional.conv2d(img.bfloat16().float(), wpe, frame.pe_b, stride=16)
+    ref = ref.permute(0, 2, 3, 1).reshape(-1, cfg.d) + frame.pos.repeat(2, 1)
+    assert float((x0 - ref).norm() / ref.norm()) < 1e-4
+    rows = torch.randn(2 * 4096, cfg.d, device="cuda")
+    out = enc.neck(rows, 2)
+    t = rows.bfloat16().float().view(2, 64, 64, cfg.d).permute(0, 3, 1, 2)
+    n1 = torch.nn.functional.conv2d(t, frame.neck1_w.float().view(256, cfg.d, 1, 1))
+    n1 = torch.nn.functional.layer_norm(n1.permute(0, 2, 3, 1), (256,), frame.neck_ln1_g, frame.neck_ln1_b, 1e-6)
+    n2 = torch.nn.functional.conv2d(n1.bfloat16().float().permute(0, 3, 1, 2), frame.neck2_w.float().view(256, 256, 3, 3),
+                                    padding=1)
+    n2 = torch.nn.functional.layer_norm(n2.permute(0, 2, 3, 1), (256,), frame.neck_ln2_g, frame.neck_ln2_b, 1e-6)
+    assert float((out - n2).norm() / n2.norm()) < 1e-2

@@ -1,0 +1,256 @@
+"""Kernel-level parity on the B200 through the C ABI (marker: gpu).
+
+Integer / index / data-movement kernels are checked bit-exactly; float kernels
+against fp32 (GEMM, LN) or float64 (attention) oracles on the same bf16
+inputs, with the tolerances written in each test.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import zs_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2605_17633_b200 import kernels as K
+
+DEV = "cuda"
+
+
+def rel(a, b):
+    a = torch.as_tensor(a).double().cpu()
+    b = torch.as_tensor(b).double().cpu()
+    return float((a - b).norm() / b.norm().clamp_min(1e-300))
+
+
+# ---------------------------------------------------------------- GEMM
+@pytest.mark.parametrize("M,N,K_", [(1, 256, 64), (127, 768, 768), (300, 512, 256), (1000, 3072, 768),
+                                    (4900, 3840, 1280), (77, 1280, 5120)])
+def test_gemm_bias_bf16(M, N, K_):
+    g = torch.Generator(device=DEV).manual_seed(M + N)
+    a = torch.randn(M, K_, device=DEV, generator=g).bfloat16()
+    w = (torch.randn(N, K_, device=DEV, generator=g) / math.sqrt(K_)).bfloat16()
+    b = torch.randn(N, device=DEV, generator=g)
+    y = K.gemm(a, w, b)
+    ref = a.float() @ w.float().T + b
+    assert rel(y, ref) < 5e-3  # bf16 output rounding (2^-9) dominates
+
+
+def test_gemm_gelu_epilogue():
+    g = torch.Generator(device=DEV).manual_seed(3)
+    a = torch.randn(333, 512, device=DEV, generator=g).bfloat16()
+    w = (torch.randn(2048, 512, device=DEV, generator=g) / 20).bfloat16()
+    b = torch.randn(2048, device=DEV, generator=g)
+    y = K.gemm(a, w, b, epi=K.EPI_BF16_GELU)
+    ref = torch.nn.functional.gelu(a.float() @ w.float().T + b)  # exact-erf GELU
+    assert rel(y, ref) < 5e-3
+
+
+def test_gemm_residual_scatter_zero_rows_and_device_m():
+    g = torch.Generator(device=DEV).manual_seed(4)
+    M, N, K_ = 333, 768, 512
+    a = torch.randn(M, K_, device=DEV, generator=g).bfloat16()
+    w = (torch.randn(N, K_, device=DEV, generator=g) / 20).bfloat16()
+    b = torch.randn(N, device=DEV, generator=g)
+    x = torch.randn(500, N, device=DEV, generator=g)
+    x0 = x.clone()
+    rm = torch.randperm(500, device=DEV, generator=g)[:M].int()
+    zr = (torch.rand(M, device=DEV, generator=g) < 0.2).to(torch.uint8)
+    mdev = torch.tensor([250], device=DEV, dtype=torch.int32)
+    K.gemm(a, w, b, epi=K.EPI_F32_RESID, out=x, res=x, row_map=rm, zero_rows=zr, m_dev=mdev)
+    ref = x0.clone()
+    live = torch.arange(M, device=DEV) < 250
+    upd = x0[rm.long()] + a.float() @ w.float().T + b
+    upd[zr.bool()] = 0
+    ref[rm.long()[live]] = upd[live]
+    assert rel(x, ref) < 1e-5  # fp32 output: accumulation order only
+    untouched = torch.ones(500, dtype=torch.bool, device=DEV)
+    untouched[rm.long()[live]] = False
+    assert torch.equal(x[untouched], x0[untouched])
+
+
+def test_gemm_residual_modulo_rows():
+    g = torch.Generator(device=DEV).manual_seed(5)
+    a = torch.randn(3 * 64, 256, device=DEV, generator=g).bfloat16()
+    w = (torch.randn(256, 256, device=DEV, generator=g) / 16).bfloat16()
+    pos = torch.randn(64, 256, device=DEV, generator=g)
+    y = K.gemm(a, w, None, epi=K.EPI_F32_RESID, res=pos, res_mod=64)
+    ref = a.float() @ w.float().T + pos.repeat(3, 1)
+    assert rel(y, ref) < 1e-5
+
+
+def test_gemm_rejects_bad_shapes():
+    a = torch.zeros(8, 100, device=DEV, dtype=torch.bfloat16)
+    w = torch.zeros(64, 100, device=DEV, dtype=torch.bfloat16)
+    with pytest.raises(RuntimeError, match="zs_status -2"):
+        K.gemm(a, w)
+
+
+# ---------------------------------------------------------------- LN / permute / maps
+def test_layernorm_rows_gather():
+    g = torch.Generator(device=DEV).manual_seed(6)
+    x = torch.randn(500, 1280, device=DEV, generator=g) * 3 + 1
+    gam = torch.randn(1280, device=DEV, generator=g)
+    bet = torch.randn(1280, device=DEV, generator=g)
+    rows = torch.randperm(500, device=DEV, generator=g)[:200].int()
+    y = K.layernorm_rows(x, gam, bet, rows, out_f32=True)
+    ref = O.layernorm(x[rows.long()].cpu().numpy(), gam.cpu().numpy(), bet.cpu().numpy())
+    assert rel(y, ref) < 1e-5
+    yb = K.layernorm_rows(x, gam, bet, rows)
+    assert rel(yb, ref) < 5e-3
+
+
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_permute_rows_exact(dtype):
+    dt = getattr(torch, dtype)
+    src = torch.randn(300, 1280, device=DEV).to(dt)
+    mp = torch.randint(-1, 300, (777,), device=DEV, dtype=torch.int32)
+    out = K.permute_rows(src, mp)
+    ref = torch.zeros(777, 1280, device=DEV, dtype=dt)
+    ok = mp >= 0
+    ref[ok] = src[mp[ok].long()]
+    assert torch.equal(out, ref)
+
+
+def test_cast_rows_bf16_exact():
+    src = torch.randn(300, 256, device=DEV)
+    assert torch.equal(K.cast_rows_bf16(src), src.bfloat16())
+
+
+def test_layout_maps_match_oracle_window_split():
+    """Maps reproduce _pad_grid/_split_windows∘sigma and sigma_g exactly (encoder.py:232-254)."""
+    rng = np.random.default_rng(0)
+    B, H, W, win = 2, 20, 20, 6
+    nwin = 16
+    sig_l = np.stack([rng.permutation(win * win) for _ in range(B * nwin)]).astype(np.int32)
+    sig_g = np.stack([rng.permutation(H * W) for _ in range(B)]).astype(np.int32)
+    m = K.layout_maps(torch.from_numpy(sig_g).to(DEV), torch.from_numpy(sig_l).to(DEV), B, H, W, win)
+    tok = np.arange(B * H * W).reshape(B, H, W, 1).astype(np.float32)
+    exp_l = []
+    for b in range(B):
+        wins = O.split_windows(O.pad_grid(tok[b] + 1, win), win)  # +1 so pads (0) are distinguishable
+        for wi in range(nwin):
+            exp_l.append(wins[wi, sig_l[b * nwin + wi], 0] - 1)
+    exp_l = np.concatenate(exp_l).astype(np.int64)
+    got_l = m["l_from_s"].cpu().numpy()
+    assert np.array_equal(got_l, exp_l)
+    assert np.array_equal(m["l_is_pad"].cpu().numpy().astype(bool), exp_l < 0)
+    exp_g = (sig_g + np.arange(B)[:, None] * H * W).reshape(-1)
+    assert np.array_equal(m["g_from_s"].cpu().numpy(), exp_g)
+    # round trips: S -> L -> G -> S and S -> G -> L -> S are identities on real tokens
+    s = torch.arange(B * H * W, device=DEV, dtype=torch.float32)[:, None].repeat(1, 4).contiguous()
+    L = K.permute_rows(s, m["l_from_s"])
+    G = K.permute_rows(L, m["g_from_l"])
+    assert torch.equal(G, K.permute_rows(s, m["g_from_s"]))
+    assert torch.equal(K.permute_rows(G, m["s_from_g"]), s)
+    assert torch.equal(K.permute_rows(K.permute_rows(G, m["l_from_g"]), m["s_from_l"]), s)
+    assert torch.equal(K.permute_rows(L, m["s_from_l"]), s)
+
+
+def test_keep_rows_prefix_skips_pads():
+    U, S, Kc = 37, 196, 78
+    rng = np.random.default_rng(1)
+    pad = (rng.random(U * S) < 0.2).astype(np.uint8)
+    keep, offs = K.prefix_keep_rows(U, S, Kc, torch.from_numpy(pad).to(DEV))
+    n = int(offs[U])
+    exp = np.array([u * S + i for u in range(U) for i in range(Kc) if not pad[u * S + i]])
+    assert n == exp.size
+    assert np.array_equal(keep[:n].cpu().numpy(), exp)
+    byp, boff = K.unit_span_rows(U, S, Kc, S, torch.from_numpy(pad).to(DEV))
+    expb = np.array([u * S + i for u in range(U) for i in range(Kc, S) if not pad[u * S + i]])
+    assert int(boff[U]) == expb.size and np.array_equal(byp[: expb.size].cpu().numpy(), expb)
+
+
+# ---------------------------------------------------------------- ordering (bit-exact)
+def test_sobel_and_orderings_bitexact_small_all_variants():
+    g = golden("orders_small")
+    x = O.SplitMix(1).normal((20, 20, 24))
+    xt = torch.from_numpy(x).to(DEV)[None].contiguous()
+    sg, sw = K.sobel_saliency(xt, 6)
+    assert np.array_equal(sg[0].cpu().numpy(), g["small_sobel"])
+    wins = O.split_windows(O.pad_grid(x, 6), 6)
+    for wi in range(wins.shape[0]):
+        assert np.array_equal(sw[0, wi].cpu().numpy(), O.sobel_magnitude(wins[wi].reshape(6, 6, -1)).reshape(-1))
+    mg = torch.from_numpy(O.morton_order(20, 20)).int().to(DEV)
+    mw = torch.from_numpy(O.morton_order(6, 6)).int().to(DEV)
+    for gran in ("zgroup", "token"):
+        for var in ("full", "no_interleave", "no_sort"):
+            s1, _ = K.rank_order(sg.reshape(1, -1), mg, granularity=gran, variant=var)
+            s2, _ = K.rank_order(sw.reshape(16, -1), mw, granularity=gran, variant=var)
+            assert np.array_equal(s1[0].cpu().numpy(), g[f"small_{gran}_{var}_global"]), (gran, var)
+            assert np.array_equal(s2.cpu().numpy(), g[f"small_{gran}_{var}_local"]), (gran, var)
+
+
+def test_orderings_bitexact_config1():
+    """Config 1 input (64x64x768, zstripe.Rng(1)): sigma_global and all 25 sigma_w bit-exact."""
+    g = golden("orders_config1")
+    x = O.SplitMix(1).normal((64, 64, 768))
+    xt = torch.from_numpy(x).to(DEV)[None].contiguous()
+    sg, sw = K.sobel_saliency(xt, 14)
+    assert np.array_equal(sg[0].cpu().numpy()[::7], g["sobel_rows"])
+    s1, _ = K.rank_order(sg.reshape(1, -1), torch.from_numpy(O.morton_order(64, 64)).int().to(DEV))
+    s2, _ = K.rank_order(sw.reshape(25, -1), torch.from_numpy(O.morton_order(14, 14)).int().to(DEV))
+    assert np.array_equal(s1[0].cpu().numpy(), g["sigma_global"])
+    assert np.array_equal(s2.cpu().numpy(), g["sigma_local"])
+
+
+def test_rank_from_reference_energies_bitexact():
+    """Top-K index sets are bit-exact when fed the reference's scores (north star)."""
+    g = golden("orders_small")
+    e = torch.from_numpy(g["small_energy"]).to(DEV)[None]
+    mg = torch.from_numpy(O.morton_order(20, 20)).int().to(DEV)
+    sig, _ = K.rank_order(e, mg, variant="no_interleave", scores_are_energy=True)
+    assert np.array_equal(sig[0].cpu().numpy(), g["small_pi"])
+
+
+def test_rank_ties_and_nan_follow_numpy_lexsort():
+    # ties -> ascending group index; NaN sorts last (numpy lexsort on -energy)
+    e = np.array([1.0, 3.0, 3.0, np.nan, 0.0, 3.0, -0.0, np.nan], np.float32)
+    morton = np.arange(32)
+    exp = O.order_from_energy(e, morton, 4)
+    sig, _ = K.rank_order(torch.from_numpy(e).to(DEV)[None], torch.from_numpy(morton).int().to(DEV),
+                          variant="no_interleave", scores_are_energy=True)
+    assert np.array_equal(sig[0].cpu().numpy(), exp)
+
+
+# ---------------------------------------------------------------- attention
+def _attn_case(units, heads, S, dh, w, tile, r, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    C = heads * dh
+    qkv = torch.randn(units * S, 3 * C, generator=g).bfloat16().to(DEV)
+    bh = (0.5 * torch.randn(heads, S, w, generator=g)).to(DEV)
+    bw = (0.5 * torch.randn(heads, S, w, generator=g)).to(DEV)
+    sp = torch.stack([torch.randperm(S, generator=g) for _ in range(units)]).int().to(DEV)
+    T = -(-S // tile)
+    out = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], units=units, heads=heads, sq=S, sk=S, dh=dh,
+                        bh=bh, bw=bw, q_sp=sp, k_sp=sp, b_row=tile, b_col=tile, prefix=math.floor(r * T),
+                        tau=1 / math.sqrt(dh))
+    qkvf = qkv.float().cpu().numpy()
+    worst = 0.0
+    for u in {0, units - 1}:
+        for h in range(heads):
+            rows = slice(u * S, (u + 1) * S)
+            s = sp[u].cpu().numpy().astype(np.int64)
+            ref = O.masked_attention_f64(qkvf[rows, h * dh:(h + 1) * dh], qkvf[rows, C + h * dh:C + (h + 1) * dh],
+                                         qkvf[rows, 2 * C + h * dh:2 * C + (h + 1) * dh], bh[h].cpu().numpy(),
+                                         bw[h].cpu().numpy(), s, s, tile, tile, r)
+            worst = max(worst, rel(out[rows, h * dh:(h + 1) * dh].float(), ref))
+    return worst
+
+
+@pytest.mark.parametrize("dh", [64, 80])
+@pytest.mark.parametrize("r", [0.0, 0.2, 0.4, 0.6, 1.0])
+def test_attention_local_window(dh, r):
+    # tolerance: bf16 P and bf16 output vs float64 softmax -> ~2e-3 relative
+    assert _attn_case(5, 2, 196, dh, 14, 32, r) < 1e-2
+
+
+@pytest.mark.parametrize("dh", [64, 80])
+@pytest.mark.parametrize("r", [0.2, 0.4, 1.0])
+def test_attention_global(dh, r):
+    assert _attn_case(2, 2, 4096, dh, 64, 128, r) < 1e-2
