@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(gemm::kThreads, 1)
                    int N, int K, GemmEpi ep) {
   using namespace gemm;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared space
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * STAGE_BYTES);
   uint64_t* full = bars;                  // [kStages]
   uint64_t* empty = bars + kStages;       // [kStages]

@@ -254,3 +254,33 @@ def test_attention_local_window(dh, r):
 @pytest.mark.parametrize("r", [0.2, 0.4, 1.0])
 def test_attention_global(dh, r):
     assert _attn_case(2, 2, 4096, dh, 64, 128, r) < 1e-2
+
+
+@pytest.mark.parametrize("dh", [64, 80])
+def test_attention_many_items_per_cta(dh):
+    """More work items than SMs: every persistent CTA walks several (unit, head, block) items,
+    so the Q / K / V / metadata rings run across item boundaries."""
+    assert _attn_case(300, 3, 196, dh, 14, 32, 0.4, seed=1) < 1e-2
+    assert _attn_case(5, 8, 4096, dh, 64, 128, 0.4, seed=2) < 1e-2
+
+
+def test_attention_general_tiles_many_items():
+    """Tile sizes that are not multiples of 32 take the per-element mask path."""
+    g = torch.Generator().manual_seed(9)
+    units, heads, S, dh, w = 200, 2, 81, 64, 9
+    C = heads * dh
+    qkv = torch.randn(units * S, 3 * C, generator=g).bfloat16().to(DEV)
+    bh = (0.5 * torch.randn(heads, S, w, generator=g)).to(DEV)
+    bw = (0.5 * torch.randn(heads, S, w, generator=g)).to(DEV)
+    sp = torch.stack([torch.randperm(S, generator=g) for _ in range(units)]).int().to(DEV)
+    for br, bc, r in [(16, 24, 0.4), (7, 5, 0.3), (81, 81, 1.0)]:
+        tc = -(-S // bc)
+        out = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], units=units, heads=heads, sq=S, sk=S, dh=dh,
+                            bh=bh, bw=bw, q_sp=sp, k_sp=sp, b_row=br, b_col=bc, prefix=math.floor(r * tc), tau=0.125)
+        qf = qkv.float().cpu().numpy()
+        for u in (0, units - 1):
+            rows = slice(u * S, (u + 1) * S)
+            s = sp[u].cpu().numpy().astype(np.int64)
+            ref = O.masked_attention_f64(qf[rows, :dh], qf[rows, C:C + dh], qf[rows, 2 * C:2 * C + dh],
+                                         bh[0].cpu().numpy(), bw[0].cpu().numpy(), s, s, br, bc, r, 0.125)
+            assert rel(out[rows, :dh].float(), ref) < 1e-2, (br, bc, r)
