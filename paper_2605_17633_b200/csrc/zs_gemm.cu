@@ -20,6 +20,8 @@
 //   warps 4..7  epilogue       tcgen05.ld -> bias/GELU/residual -> global
 // TMEM holds two 128x256 fp32 accumulators so the epilogue of tile i overlaps
 // the MMAs of tile i+1.
+#include <cstdlib>
+
 #include "zs_common.cuh"
 #include "zs_host.h"
 
@@ -233,6 +235,9 @@ __global__ void __launch_bounds__(gemm::kThreads, 1)
 
 namespace zs {
 
+int launch_gemm2(int epi, const void* A, long long lda, const void* W, long long ldw, int M, int N, int K,
+                 const GemmEpi& ep, cudaStream_t stream);
+
 int launch_gemm(int epi, const void* A, long long lda, const void* W, long long ldw, int M, int N, int K,
                 const GemmEpi& ep, cudaStream_t stream, int max_ctas) {
   using namespace gemm;
@@ -240,6 +245,10 @@ int launch_gemm(int epi, const void* A, long long lda, const void* W, long long 
   if (N <= 0 || K <= 0 || (K % BK) != 0 || (N % 32) != 0) return ZS_ERR_SHAPE;
   if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(W) & 15) || (lda % 8) || (ldw % 8))
     return ZS_ERR_ALIGN;
+  if (epi < 0 || epi > 2) return ZS_ERR_ARG;
+  // CTA-pair kernel for everything but tiny problems (ZS_GEMM_1CTA=1 forces the single-CTA kernel)
+  static const bool force_1cta = getenv("ZS_GEMM_1CTA") != nullptr;
+  if (!force_1cta && max_ctas <= 0 && M > 128) return launch_gemm2(epi, A, lda, W, ldw, M, N, K, ep, stream);
   CUtensorMap ta, tb;
   int rc = make_tmap_2d_bf16(&ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B);
   if (rc) return rc;
