@@ -124,6 +124,11 @@ ZS_API int zs_unit_span_rows(int U, int S, int begin, int end, const uint8_t* is
  * replaces: tensor.py:214-236 `layernorm` (as used at encoder.py:289, mlp.py:82,110). */
 ZS_API int zs_layernorm_rows(const float* x, long long ldx, const int32_t* rows, long long n, int C, const float* gamma,
                       const float* beta, float eps, void* out, long long ldo, int out_f32, zs_stream_t stream);
+/* Extended form: output row i goes to out_rows[i] (NULL = i) and only the first
+ * min(n, *n_dev) rows are processed when n_dev is given (device-side count). */
+ZS_API int zs_layernorm_rows_ex(const float* x, long long ldx, const int32_t* rows, const int32_t* out_rows, long long n,
+                         const int32_t* n_dev, int C, const float* gamma, const float* beta, float eps, void* out,
+                         long long ldo, int out_f32, zs_stream_t stream);
 
 /* --------------------------------------------------------------------- GEMM
  * tcgen05 GEMM  D = A[M,K] · W[N,K]^T  (bf16, fp32 accumulate) with fused epilogue:

@@ -32,6 +32,7 @@ SIGNATURES: dict[str, list] = {
     "zs_prefix_keep_rows": [_i, _i, _i, _p, _p, _p, _p],
     "zs_unit_span_rows": [_i, _i, _i, _i, _p, _p, _p, _p],
     "zs_layernorm_rows": [_p, _ll, _p, _ll, _i, _p, _p, _f, _p, _ll, _i, _p],
+    "zs_layernorm_rows_ex": [_p, _ll, _p, _p, _ll, _p, _i, _p, _p, _f, _p, _ll, _i, _p],
     "zs_gemm_bf16": [_i, _p, _ll, _p, _ll, _i, _i, _i, _p, _p, _ll, _p, _ll, _p, _p, _i, _p, _p],
     "zs_stripe_attn_fwd": [_p, _p, _p, _ll, _ll, _ll, _ll, _ll, _i, _i, _i, _i, _i, _p, _p, _i, _p, _p, _i, _i,
                            _i, _f, _p, _ll, _ll, _p],

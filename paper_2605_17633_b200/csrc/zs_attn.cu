@@ -66,6 +66,7 @@ struct Params {
   // key tile of every 32-key group, precomputed on the host so the hot loops never divide
   unsigned char ck_lo[64], ck_hi[64];
   unsigned char gkt[256];
+  unsigned long long mbmask[64];  // needed-chunk bitmask of every 128-row query block
 };
 
 template <int DH>
@@ -81,9 +82,9 @@ struct Layout {
   static constexpr int OFF_XMAX = OFF_KOFF + 2 * BKC * 8;  // [chunk parity][half][BQ]
   static constexpr int OFF_XSUM = OFF_XMAX + 4 * BQ * 4;
   static constexpr int OFF_BAR = OFF_XSUM + 4 * BQ * 4;   // xsum: [chunk parity][half][BQ]
-  static constexpr int OFF_TAB = OFF_BAR + 512;           // ck_lo[64] ck_hi[64] gkt[256]
-  static constexpr int OFF_Q = OFF_BAR + 1024;            // q_slots x TILE (1024-aligned)
-  static_assert(OFF_TAB + 384 <= OFF_Q, "table region overflows");
+  static constexpr int OFF_TAB = OFF_BAR + 512;           // ck_lo[64] ck_hi[64] gkt[256] | mbmask[64] at +512
+  static constexpr int OFF_Q = OFF_BAR + 2048;            // q_slots x TILE (1024-aligned)
+  static_assert(OFF_TAB + 1024 <= OFF_Q, "table region overflows");
   static constexpr int TX_Q = BQ * DH * 2;
   static constexpr int TX_KV = BKC * DH * 2;
   static int off_bias(int q_slots) { return OFF_Q + q_slots * TILE; }
@@ -96,9 +97,11 @@ struct Layout {
 template <bool FAST>
 struct ChunkPlan {
   int nck, p, tc, bcol, dlo, dhi;
-  const unsigned char* lo;  // shared-memory copies of Params::ck_lo / ck_hi
+  const unsigned char* lo;  // shared-memory copies of Params::ck_lo / ck_hi / mbmask
   const unsigned char* hi;
+  const unsigned long long* mbm;
   __device__ __forceinline__ void init(const Params& P, int row0) {
+    if constexpr (FAST) mask = mbm[row0 / BQ];
     nck = (P.sk + BKC - 1) / BKC;
     p = P.prefix;
     tc = P.tc;
@@ -120,7 +123,12 @@ struct ChunkPlan {
     if (kt_lo < p) return true;
     return !(dhi < kt_lo || dlo > kt_hi);
   }
+  unsigned long long mask;  // FAST: needed-chunk bitmask of this query block (from the smem table)
   __device__ __forceinline__ int next(int cj) const {  // next needed chunk after cj, or -1
+    if constexpr (FAST) {
+      const unsigned long long rest = (cj + 1 >= 64) ? 0ull : (mask >> (cj + 1)) << (cj + 1);
+      return rest ? __ffsll((long long)rest) - 1 : -1;
+    }
     for (int j = cj + 1; j < nck; ++j)
       if (needed(j)) return j;
     return -1;
@@ -136,6 +144,7 @@ struct Cursor {
   __device__ __forceinline__ void init_tables(const unsigned char* tab) {
     plan.lo = tab;
     plan.hi = tab + 64;
+    plan.mbm = reinterpret_cast<const unsigned long long*>(tab + 512);
   }
   __device__ __forceinline__ void load_item(const Params& P) {
     valid = it < P.items;
@@ -172,9 +181,12 @@ struct Cursor {
 
 // wait with a short sleep between probes: for the single-lane producer / MMA / loader warps, so their
 // spinning does not steal issue slots from the softmax warps sharing the SM sub-partitions
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  while (!mbar_try_wait(a, parity)) __nanosleep(32);
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) { mbar_wait_sleep(bar, parity); }
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
@@ -253,6 +265,7 @@ __global__ void __launch_bounds__(attn::kThreads, 1)
     unsigned char* tab = smem + L::OFF_TAB;
     for (int i = threadIdx.x; i < 384; i += blockDim.x)
       tab[i] = i < 64 ? P.ck_lo[i] : (i < 128 ? P.ck_hi[i - 64] : P.gkt[i - 128]);
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) reinterpret_cast<unsigned long long*>(tab + 512)[i] = P.mbmask[i];
   }
   tc_fence_before();
   __syncthreads();
@@ -508,7 +521,6 @@ __global__ void __launch_bounds__(attn::kThreads, 1)
           tmem_ld32(s_addr + g * 32, sr);
           tmem_ld_wait();
           if constexpr (FAST) {
-            const bool ragged = c0 + 32 > P.sk;
 #pragma unroll
             for (int j = 0; j < 32; j += 2) {
               const int4 oo = *reinterpret_cast<const int4*>(ko + g * 32 + j);
@@ -516,14 +528,16 @@ __global__ void __launch_bounds__(attn::kThreads, 1)
               float x1 = fmaf(P.tau, __uint_as_float(sr[j + 1]), *reinterpret_cast<const float*>(bh_row + oo.z));
               x0 += *reinterpret_cast<const float*>(bw_row + oo.y);
               x1 += *reinterpret_cast<const float*>(bw_row + oo.w);
-              if (ragged) {
-                if (c0 + j >= P.sk) x0 = -INFINITY;
-                if (c0 + j + 1 >= P.sk) x1 = -INFINITY;
-              }
-              mx = fmaxf(mx, fmaxf(x0, x1));
               sr[j] = __float_as_uint(x0);
               sr[j + 1] = __float_as_uint(x1);
             }
+            if (c0 + 32 > P.sk) {  // ragged last group (warp-uniform, rare)
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (c0 + j >= P.sk) sr[j] = __float_as_uint(-INFINITY);
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) mx = fmaxf(mx, __uint_as_float(sr[j]));
           } else {
 #pragma unroll 4
             for (int j = 0; j < 32; ++j) {
@@ -563,7 +577,7 @@ __global__ void __launch_bounds__(attn::kThreads, 1)
       float alpha = 1.f;
       bool resc = false;
       if (mrow > m_ref + kRescaleThr || (m_ref == -INFINITY && mrow > -INFINITY)) {
-        alpha = (m_ref == -INFINITY) ? 0.f : exp2f((m_ref - mrow) * L2E);
+        alpha = (m_ref == -INFINITY) ? 0.f : ex2((m_ref - mrow) * L2E);
         resc = !cu.first;
         m_ref = mrow;
       }
@@ -601,7 +615,7 @@ __global__ void __launch_bounds__(attn::kThreads, 1)
             float pj[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-              pj[j] = exp2f(fmaf(__uint_as_float(sr[8 * q8 + j]), L2E, -mb2));
+              pj[j] = ex2(fmaf(__uint_as_float(sr[8 * q8 + j]), L2E, -mb2));
               rs += pj[j];
             }
             w4[q8].x = pack_bf16(pj[0], pj[1]);
@@ -709,7 +723,8 @@ static int launch_attn_dh(const void* q, const void* k, const void* v, long long
   if (rc) return ZS_ERR_TMAP;
   const int nck = (p.sk + attn::BKC - 1) / attn::BKC;
   const int ngroups = (p.sk + 31) / 32;
-  const bool fast = (p.b_row % 32) == 0 && (p.b_col % 32) == 0 && nck <= 64 && ngroups <= 256 && p.tc <= 255;
+  const bool fast = (p.b_row % 32) == 0 && (p.b_col % 32) == 0 && nck <= 64 && ngroups <= 256 && p.tc <= 255 &&
+                    p.nmb <= 64;
   if (fast) {
     for (int cj = 0; cj < 64; ++cj) {
       const int lo = (cj * attn::BKC) / p.b_col;
@@ -718,6 +733,17 @@ static int launch_attn_dh(const void* q, const void* k, const void* v, long long
       p.ck_hi[cj] = (unsigned char)std::max(0, std::min(hi, 255));
     }
     for (int g = 0; g < 256; ++g) p.gkt[g] = (unsigned char)std::min((g * 32) / p.b_col, 255);
+    for (int mb = 0; mb < 64; ++mb) {
+      unsigned long long msk = 0;
+      const int r0 = mb * attn::BQ;
+      if (r0 < p.sq) {
+        const int dlo = std::min(r0 / p.b_row, p.tc - 1);
+        const int dhi = std::min(std::min(r0 + attn::BQ - 1, p.sq - 1) / p.b_row, p.tc - 1);
+        for (int cj = 0; cj < nck; ++cj)
+          if (p.ck_lo[cj] < p.prefix || !(dhi < p.ck_lo[cj] || dlo > p.ck_hi[cj])) msk |= 1ull << cj;
+      }
+      p.mbmask[mb] = msk;
+    }
     return launch_attn<DH, true>(m, p, st);
   }
   return launch_attn<DH, false>(m, p, st);

@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(gemm::kThreads, 1)
         const int m0 = (t / n_tiles) * BM;
         const int n0 = (t % n_tiles) * BN;
         for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait_sleep(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
           mbar_expect_tx(&full[stage], STAGE_BYTES);
@@ -112,11 +112,11 @@ __global__ void __launch_bounds__(gemm::kThreads, 1)
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       const int as = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
-      mbar_wait(&tempty[as], aphase ^ 1);
+      mbar_wait_sleep(&tempty[as], aphase ^ 1);
       tc_fence_after();
       const uint32_t dtm = tmem_base + as * BN;
       for (int kb = 0; kb < nk; ++kb) {
-        mbar_wait(&full[stage], phase);
+        mbar_wait_sleep(&full[stage], phase);
         tc_fence_after();
         if (lane == 0) {
           uint8_t* sa = smem + stage * STAGE_BYTES;
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(gemm::kThreads, 1)
       const uint32_t aphase = (it >> 1) & 1;
       const int m0 = (t / n_tiles) * BM;
       const int n0 = (t % n_tiles) * BN;
-      mbar_wait(&tfull[as], aphase);
+      mbar_wait_sleep(&tfull[as], aphase);
       tc_fence_after();
       const int m = m0 + q * 32 + lane;
       const bool valid = m < M;

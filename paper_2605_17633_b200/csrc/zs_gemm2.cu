@@ -147,7 +147,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
         const int m0 = (t / n_tiles) * 2 * BM + rank * BM;
         const int n0 = (t % n_tiles) * BN + rank * BNH;
         for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait_sleep(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
           if (leader)
@@ -171,11 +171,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
       int it = 0;
       for (int t = cid; t < num_tiles; t += ncl, ++it) {
         const int as = it & 1;
-        mbar_wait(&tempty[as], ((it >> 1) & 1) ^ 1);
+        mbar_wait_sleep(&tempty[as], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t dtm = tmem_base + as * BN;
         for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait_sleep(&full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
             uint8_t* sa = smem + stage * STAGE_BYTES;
@@ -204,7 +204,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
       const int as = it & 1;
       const int m0 = (t / n_tiles) * 2 * BM + rank * BM;
       const int n0 = (t % n_tiles) * BN;
-      mbar_wait(&tfull[as], (it >> 1) & 1);
+      mbar_wait_sleep(&tfull[as], (it >> 1) & 1);
       tc_fence_after();
       const int m = m0 + q * 32 + lane;
       const bool valid = m < M;

@@ -312,6 +312,12 @@ extern "C" int zs_layernorm_rows(const float* x, long long ldx, const int32_t* r
   return launch_layernorm(x, ldx, rows, nullptr, n, nullptr, C, gamma, beta, eps, out, ldo, out_f32, S(stream));
 }
 
+extern "C" int zs_layernorm_rows_ex(const float* x, long long ldx, const int32_t* rows, const int32_t* out_rows,
+                                    long long n, const int32_t* n_dev, int C, const float* gamma, const float* beta,
+                                    float eps, void* out, long long ldo, int out_f32, zs_stream_t stream) {
+  return launch_layernorm(x, ldx, rows, out_rows, n, n_dev, C, gamma, beta, eps, out, ldo, out_f32, S(stream));
+}
+
 extern "C" int zs_permute_rows_f32(const float* src, float* dst, const int32_t* map, long long rows_out, int C,
                                    zs_stream_t stream) {
   if (rows_out <= 0) return 0;

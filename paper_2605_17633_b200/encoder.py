@@ -181,7 +181,7 @@ class StripeSortEncoder:
         w = blk.bh.shape[-1]
         with tr.span("layernorm", bytes=R * C * 6):
             h = K.layernorm_rows(xs, blk.ln1_g, blk.ln1_b, out=ws["h"][:R])
-        with tr.span("gemm", flops=2.0 * R * C * 3 * C, bytes=R * C * 2 + 3 * C * C * 2 + R * 3 * C * 2):
+        with tr.span("gemm_qkv", flops=2.0 * R * C * 3 * C, bytes=R * C * 2 + 3 * C * C * 2 + R * 3 * C * 2):
             qkv = K.gemm(h, blk.qkv_w, blk.qkv_b, out=ws["qkv"][:R])
         E = attention_elements(S, tile, prefix)
         with tr.span(f"attn_{blk.kind}", flops=4.0 * dh * E * U * H,
@@ -189,14 +189,25 @@ class StripeSortEncoder:
             o = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], units=U, heads=H, sq=S, sk=S, dh=dh,
                               bh=blk.bh, bw=blk.bw, q_sp=sig, k_sp=sig, b_row=tile, b_col=tile, prefix=prefix,
                               tau=1.0 / math.sqrt(dh), out=ws["o"][:R])
-        with tr.span("gemm", flops=2.0 * R * C * C, bytes=R * C * 2 + C * C * 2 + R * C * 8):
+        with tr.span("gemm_proj", flops=2.0 * R * C * C, bytes=R * C * 2 + C * C * 2 + R * C * 8):
             K.gemm(o, blk.proj_w, blk.proj_b, epi=K.EPI_F32_RESID, out=xs, res=xs,
                    zero_rows=od.maps["l_is_pad"] if local else None)
+        # RC-MLP (mlp.py:88-114): gather-LN of the kept rows -> fc1 + GELU -> fc2 + scatter-add residual
         nk = rows["n_keep"]
-        with tr.span("rc_mlp", flops=(nk, 16.0 * C * C), bytes=(nk, C * 4 * 2 + C * 2 + 8 * C * 2)):
-            K.rc_mlp(xs, rows["keep"], n_keep_dev=nk, ln_g=blk.ln2_g, ln_b=blk.ln2_b, w1=blk.w1, b1=blk.b1,
-                     w2=blk.w2, b2=blk.b2, bypass_rows=rows.get("bypass"), n_bypass_dev=rows.get("n_bypass"),
-                     ws=ws["mlp"])
+        mk = rows["max_keep"]
+        hidden = blk.w1.shape[0]
+        hln = ws["mlp"][: mk * C].view(mk, C)
+        hid = ws["mlp"][mk * C: mk * (C + hidden)].view(mk, hidden)
+        with tr.span("mlp_ln", bytes=(nk, C * 6)):
+            K.layernorm_rows(xs, blk.ln2_g, blk.ln2_b, rows["keep"], out=hln, n_dev=nk)
+        with tr.span("gemm_fc1", flops=(nk, 2.0 * C * hidden)):
+            K.gemm(hln, blk.w1, blk.b1, epi=K.EPI_BF16_GELU, out=hid, m_dev=nk)
+        with tr.span("gemm_fc2", flops=(nk, 2.0 * C * hidden)):
+            K.gemm(hid, blk.w2, blk.b2, epi=K.EPI_F32_RESID, out=xs, res=xs, row_map=rows["keep"], m_dev=nk)
+        if "bypass" in rows:
+            with tr.span("mlp_ln", bytes=(rows["n_bypass"], C * 8)):
+                K.layernorm_rows(xs, blk.ln2_g, blk.ln2_b, rows["bypass"], out_f32=True, out=xs,
+                                 out_rows=rows["bypass"], n_dev=rows["n_bypass"])
 
     def forward_rows(self, x0: torch.Tensor, mode: str = "sparse", orderings: Orderings | None = None,
                      out: torch.Tensor | None = None) -> torch.Tensor:

@@ -95,6 +95,8 @@ def layernorm_rows(
     eps: float = 1e-6,
     out_f32: bool = False,
     out: torch.Tensor | None = None,
+    out_rows: torch.Tensor | None = None,
+    n_dev: torch.Tensor | None = None,
 ) -> torch.Tensor:
     _need(x, torch.float32, "x")
     _need(gamma, torch.float32, "gamma")
@@ -105,8 +107,12 @@ def layernorm_rows(
         _need(rows, torch.int32, "rows")
     if out is None:
         out = torch.empty((n, C), device=x.device, dtype=torch.float32 if out_f32 else torch.bfloat16)
-    _lib.call("zs_layernorm_rows", _ptr(x), x.stride(0), _ptr(rows), n, C, _ptr(gamma), _ptr(beta), eps, _ptr(out),
-              out.stride(0), int(out_f32), _stream())
+    if n_dev is not None or out_rows is not None:
+        _lib.call("zs_layernorm_rows_ex", _ptr(x), x.stride(0), _ptr(rows), _ptr(out_rows), n, _ptr(n_dev), C,
+                  _ptr(gamma), _ptr(beta), eps, _ptr(out), out.stride(0), int(out_f32), _stream())
+    else:
+        _lib.call("zs_layernorm_rows", _ptr(x), x.stride(0), _ptr(rows), n, C, _ptr(gamma), _ptr(beta), eps,
+                  _ptr(out), out.stride(0), int(out_f32), _stream())
     return out
 
 

@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests -q -x -m gpu -k "encoder or mlp or route" 2>&1 | tail -3
+timeout 900 python bench.py --steps 5 --warmup 3 --no-cpu --no-dense > gpurun_out/bench13.log 2>&1
+tail -1 gpurun_out/bench13.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['e2e']['value'], d['roofline']); [print(k, round(v['ms_per_step'],2), v.get('tflops'), v.get('gbs')) for k,v in d['kernels'].items()]"
