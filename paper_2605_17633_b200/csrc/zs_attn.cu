@@ -388,16 +388,18 @@ __global__ void __launch_bounds__(attn::kThreads, 1)
     cu.start(P);
     while (cu.valid) {
       const int c = cu.c, st = c & 1;
-      mbar_wait_backoff(&ki_empty[st], ((c >> 1) & 1) ^ 1);
-      for (int j = lane; j < BKC; j += 32) {
-        const int kg = cu.cj * BKC + j;
-        int2 o2 = make_int2(0, 0);
-        if (kg < P.sk) {
-          const int ksp = P.k_sp[(long long)cu.u * P.sk + kg];
-          o2 = make_int2((ksp / P.bias_w) * 4, (ksp % P.bias_w) * 4);
-        }
-        koff[st * BKC + j] = o2;
+      // the chunk's 128 key indices in flight at once (one memory latency per chunk)
+      int ksp[BKC / 32];
+#pragma unroll
+      for (int i = 0; i < BKC / 32; ++i) {
+        const int kg = cu.cj * BKC + lane + 32 * i;
+        ksp[i] = kg < P.sk ? __ldg(P.k_sp + (long long)cu.u * P.sk + kg) : -1;
       }
+      mbar_wait_backoff(&ki_empty[st], ((c >> 1) & 1) ^ 1);
+#pragma unroll
+      for (int i = 0; i < BKC / 32; ++i)
+        koff[st * BKC + lane + 32 * i] =
+            ksp[i] >= 0 ? make_int2((ksp[i] / P.bias_w) * 4, (ksp[i] % P.bias_w) * 4) : make_int2(0, 0);
       mbar_arrive(&ki_full[st]);
       cu.advance(P);
     }
@@ -673,6 +675,10 @@ __global__ void __launch_bounds__(attn::kThreads, 1)
 
 using namespace zs;
 
+int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
+                    long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
+                    const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
+                    float tau, void* out, long long ldo, long long ous, cudaStream_t st);
 int launch_attn_local(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                       long long qus, long long kvus, int units, int heads, int sq, int sk, int dh, const float* bh,
                       const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col,
@@ -793,9 +799,18 @@ extern "C" int zs_stripe_attn_fwd(const void* q, const void* k, const void* v, l
   p.off_bias = 0;
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (sq <= 256 && sk <= 256 && !getenv("ZS_ATTN_FORCE_GENERIC"))  // windows: ping-pong kernel (zs_attn_local.cu)
+  if (sq <= 256 && sk <= 256 && !getenv("ZS_ATTN_FORCE_GENERIC")) {
+    // windows: one-pass TMEM-P kernel (zs_attn_win.cu) when the schedule fits its envelope,
+    // else the ping-pong window kernel (zs_attn_local.cu)
+    if (sq == sk && !getenv("ZS_ATTN_NO_WIN")) {
+      const int rc = launch_attn_win(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, dh, bh,
+                                     bw, bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride,
+                                     st);
+      if (rc <= 0) return rc;
+    }
     return launch_attn_local(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, sk, dh, bh, bw,
                              bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride, st);
+  }
   if (dh == 64) return launch_attn_dh<64>(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, p, st);
   return launch_attn_dh<80>(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, p, st);
 }

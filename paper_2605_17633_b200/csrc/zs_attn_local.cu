@@ -233,15 +233,17 @@ __global__ void __launch_bounds__(attnl::kThreads, 1)
     for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
       const int u = it / P.heads;
       const int par = k & 1;
-      wait_sleep(&ki_empty[par], ((k >> 1) & 1) ^ 1);
-      for (int j = lane; j < 256; j += 32) {
-        int2 o2 = make_int2(0, 0);
-        if (j < P.sk) {
-          const int ksp = P.k_sp[(long long)u * P.sk + j];
-          o2 = make_int2((ksp / P.bias_w) * 4, (ksp % P.bias_w) * 4);
-        }
-        koff[par * 256 + j] = o2;
+      int ksp[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int j = lane + 32 * i;
+        ksp[i] = j < P.sk ? __ldg(P.k_sp + (long long)u * P.sk + j) : -1;
       }
+      wait_sleep(&ki_empty[par], ((k >> 1) & 1) ^ 1);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        koff[par * 256 + lane + 32 * i] =
+            ksp[i] >= 0 ? make_int2((ksp[i] / P.bias_w) * 4, (ksp[i] % P.bias_w) * 4) : make_int2(0, 0);
       mbar_arrive(&ki_full[par]);
     }
   } else {

@@ -244,10 +244,36 @@ def _attn_case(units, heads, S, dh, w, tile, r, seed=0):
 
 
 @pytest.mark.parametrize("dh", [64, 80])
-@pytest.mark.parametrize("r", [0.0, 0.2, 0.4, 0.6, 1.0])
+@pytest.mark.parametrize("r", [0.0, 0.2, 0.4, 0.6, 0.8, 1.0])
 def test_attention_local_window(dh, r):
     # tolerance: bf16 P and bf16 output vs float64 softmax -> ~2e-3 relative
     assert _attn_case(5, 2, 196, dh, 14, 32, r) < 1e-2
+
+
+@pytest.mark.parametrize("S,w,tile,r", [(100, 10, 32, 0.4), (144, 12, 32, 0.5), (225, 15, 64, 0.3), (64, 8, 32, 1.0)])
+def test_attention_window_shapes(S, w, tile, r):
+    """Single-tile windows (S <= 128), a 144-token window, 64-row tiles, odd table widths."""
+    assert _attn_case(7, 3, S, 80, w, tile, r, seed=3) < 1e-2
+    assert _attn_case(7, 2, S, 64, w, tile, r, seed=4) < 1e-2
+
+
+@pytest.mark.parametrize("r", [0.2, 0.4, 0.8])
+def test_attention_window_kernels_agree(r, monkeypatch):
+    """The one-pass TMEM-P window kernel and the ping-pong window kernel give the same
+    softmax (both within bf16 rounding of each other)."""
+    g = torch.Generator().manual_seed(11)
+    units, heads, S, dh, w = 40, 4, 196, 80, 14
+    C = heads * dh
+    qkv = torch.randn(units * S, 3 * C, generator=g).bfloat16().to(DEV)
+    bh = (0.5 * torch.randn(heads, S, w, generator=g)).to(DEV)
+    bw = (0.5 * torch.randn(heads, S, w, generator=g)).to(DEV)
+    sp = torch.stack([torch.randperm(S, generator=g) for _ in range(units)]).int().to(DEV)
+    kw = dict(units=units, heads=heads, sq=S, sk=S, dh=dh, bh=bh, bw=bw, q_sp=sp, k_sp=sp, b_row=32, b_col=32,
+              prefix=math.floor(r * 7), tau=dh ** -0.5)
+    a = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], **kw)
+    monkeypatch.setenv("ZS_ATTN_NO_WIN", "1")
+    b = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], **kw)
+    assert rel(a.float(), b.float()) < 5e-3
 
 
 @pytest.mark.parametrize("dh", [64, 80])
