@@ -323,6 +323,13 @@ __global__ void __launch_bounds__(attn::kThreads, 1)
     constexpr uint32_t id_s = idesc_bf16(BQ, BKC);
     constexpr uint32_t id_pv = idesc_bf16(BQ, 64, false, true);
     constexpr uint32_t id_pv2 = idesc_bf16(BQ, 16, false, true);
+    // descriptors hoisted out of the issue loop (uniform registers); slots / k-steps are added
+    // in 16-byte units and every MMA is issued by one elected lane of this warp
+    constexpr uint32_t TILE16 = L::TILE >> 4;
+    const uint64_t dq = sdesc_k_sw128(sQ), dqt = sdesc_k_sw32(sQ + L::MAIN);
+    const uint64_t dk = sdesc_k_sw128(sK), dkt = sdesc_k_sw32(sK + L::MAIN);
+    const uint64_t dp = sdesc_k_sw128(sP);
+    const uint64_t dv = sdesc_mn_sw128(sV), dvt = sdesc_mn_sw32(sV + L::MAIN);
     auto issue_s = [&](const Cursor<FAST>& cu) {
       const int qs = cu.k % P.q_slots;
       if (cu.first) mbar_wait_backoff(&q_full[qs], (cu.k / P.q_slots) & 1);
@@ -330,39 +337,31 @@ __global__ void __launch_bounds__(attn::kThreads, 1)
       mbar_wait_backoff(&k_full[ks_], (c / KST) & 1);
       mbar_wait_backoff(&s_empty[st], ((c >> 1) & 1) ^ 1);
       tc_fence_after();
-      if (lane == 0) {
-        uint8_t* q = sQ + qs * L::TILE;
-        uint8_t* kk = sK + ks_ * L::TILE;
-        const uint32_t d = tmem + TM_S + st * 128;
+      const uint64_t q = dq + qs * TILE16, qt = dqt + qs * TILE16;
+      const uint64_t kk = dk + ks_ * TILE16, kt = dkt + ks_ * TILE16;
+      const uint32_t d = tmem + TM_S + st * 128;
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks)
-          umma_bf16(d, sdesc_k_sw128(q) + 2 * ks, sdesc_k_sw128(kk) + 2 * ks, id_s, ks > 0);
-        if constexpr (L::kTail) umma_bf16(d, sdesc_k_sw32(q + L::MAIN), sdesc_k_sw32(kk + L::MAIN), id_s, 1);
-        umma_commit(&s_full[st]);
-        umma_commit(&k_empty[ks_]);
-        if (cu.last) umma_commit(&q_empty[qs]);
-      }
-      __syncwarp();
+      for (int ks = 0; ks < 4; ++ks) umma_ss(d, q + 2 * ks, kk + 2 * ks, id_s, ks > 0);
+      if constexpr (L::kTail) umma_ss(d, qt, kt, id_s, 1);
+      umma_commit_elect(&s_full[st]);
+      umma_commit_elect(&k_empty[ks_]);
+      if (cu.last) umma_commit_elect(&q_empty[qs]);
     };
     auto issue_pv = [&](const Cursor<FAST>& cu) {
       const int c = cu.c, vs = c % VST;
       mbar_wait_backoff(p_full, c & 1);
       mbar_wait_backoff(&v_full[vs], (c / VST) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        uint8_t* v = sV + vs * L::TILE;
+      const uint64_t v = dv + vs * TILE16, vt = dvt + vs * TILE16;
 #pragma unroll
-        for (int ks = 0; ks < BKC / 16; ++ks) {
-          const uint64_t a = sdesc_k_sw128(sP + (ks >> 2) * (BQ * 128)) + 2 * (ks & 3);
-          const uint32_t acc = (!cu.first || ks > 0) ? 1u : 0u;
-          umma_bf16(tmem + TM_O, a, sdesc_mn_sw128(v + ks * 16 * 128), id_pv, acc);
-          if constexpr (L::kTail)
-            umma_bf16(tmem + TM_O + 64, a, sdesc_mn_sw32(v + L::MAIN + ks * 16 * 32), id_pv2, acc);
-        }
-        umma_commit(pv_full);
-        umma_commit(&v_empty[vs]);
+      for (int ks = 0; ks < BKC / 16; ++ks) {
+        const uint64_t a = dp + (ks >> 2) * (BQ * 128 / 16) + 2 * (ks & 3);
+        const uint32_t acc = (!cu.first || ks > 0) ? 1u : 0u;
+        umma_ss(tmem + TM_O, a, v + ks * (16 * 128 / 16), id_pv, acc);
+        if constexpr (L::kTail) umma_ss(tmem + TM_O + 64, a, vt + ks * (16 * 32 / 16), id_pv2, acc);
       }
-      __syncwarp();
+      umma_commit_elect(pv_full);
+      umma_commit_elect(&v_empty[vs]);
     };
     Cursor<FAST> cs, cp;
     cs.init_tables(smem + L::OFF_TAB);
@@ -679,6 +678,10 @@ int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, 
                     long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
                     const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
                     float tau, void* out, long long ldo, long long ous, cudaStream_t st);
+int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
+                     long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
+                     const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
+                     float tau, void* out, long long ldo, long long ous, cudaStream_t st);
 int launch_attn_local(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                       long long qus, long long kvus, int units, int heads, int sq, int sk, int dh, const float* bh,
                       const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col,
@@ -810,6 +813,11 @@ extern "C" int zs_stripe_attn_fwd(const void* q, const void* k, const void* v, l
     }
     return launch_attn_local(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, sk, dh, bh, bw,
                              bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride, st);
+  }
+  if (sq == sk && !getenv("ZS_ATTN_NO_GLOB")) {  // 128x128 tiles: split-chunk TMEM-P kernel (zs_attn_glob.cu)
+    const int rc = launch_attn_glob(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, dh, bh, bw,
+                                    bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride, st);
+    if (rc <= 0) return rc;
   }
   if (dh == 64) return launch_attn_dh<64>(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, p, st);
   return launch_attn_dh<80>(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, p, st);

@@ -1,0 +1,663 @@
+// zs_attn_glob.cu — stripe-sort attention for the global blocks (S = 4096, 128-row query tiles,
+// 128-key tiles: encoder.py:57-58 b_global = 128).
+//
+// Semantics as zs_attn.cu (attention.py:88-104, :167-221).  With b_row = b_col = 128 every
+// work item (unit, head, query tile i) is one 128-row MMA tile and every key tile one 128-key
+// chunk, so J_i = {0..p-1} ∪ {min(i, Tc-1)} is a list of whole chunks: no intra-chunk mask
+// except keys / rows past S.
+//
+// B200 design (one persistent CTA per SM):
+//  * Two softmax warpgroups split the chunks (WG w takes the CTA's chunk ordinals c with
+//    c % 2 == w, so S(c) always targets the other WG's S buffer than S(c-1)), each
+//    with its own S buffer, O accumulator (TMEM) and running max / sum, so the two chunks'
+//    softmaxes run concurrently with no per-chunk exchange; the partial results merge once per
+//    item in the epilogue (each WG writes half of the output columns).
+//  * One thread per query row holds the 128 logits of a chunk in registers; the decomposed
+//    rel-pos bias bh[σq(r), σk/64] + bw[σq(r), σk%64] is looked up in an odd-stride fp32 row
+//    table (bank-conflict-free) staged per item by a dedicated warp with cp.async.
+//  * P (bf16) overwrites the WG's S columns in TMEM and is the A operand of the PV MMA.
+//  * Lazy rescaling: O_w is rescaled in TMEM only when the row max grows by more than ln 256.
+//  * MMA issue order S(0) S(1) PV(0) S(2) PV(1) ... keeps the tensor core busy on one WG's
+//    chunk while the other WG's softmax runs.
+// Roles: warp 0 TMA (Q per item, K / V ring per chunk), warp 1 MMA (whole warp, elected lane),
+// warp 2 TMEM owner + key metadata (σk -> bias byte offsets per chunk), warp 3 bias rows,
+// warps 4-7 WG0, warps 8-11 WG1.
+#include <algorithm>
+#include <cstdlib>
+
+#include <cuda_fp16.h>
+
+#include "zs_common.cuh"
+#include "zs_host.h"
+
+namespace zs {
+namespace attng {
+
+constexpr int BQ = 128;
+constexpr int kThreads = 384;
+constexpr uint32_t kTmemCols = 512;
+constexpr int KST = 3;  // K ring stages
+constexpr int VST = 2;  // V ring stages
+constexpr int MST = 3;  // key-metadata ring stages
+constexpr uint32_t TM_S = 0;    // S_w at [w*128, w*128+128)
+constexpr uint32_t TM_O = 256;  // O_w at 256 + w*128
+
+struct Params {
+  int units, heads, S, bias_w, W1, T, prefix, items;
+  long long ldo, o_unit_stride;
+  const __half* btab;  // [heads, S, 128] fp16 bias rows: bh in cols [0, w), bw in [64, 64 + w)
+  const int* q_sp;
+  const int* k_sp;
+  float tau;
+  __nv_bfloat16* out;
+  int off_q, off_k, off_v, off_bias, off_koff, off_ml, off_bar, tile;
+  int trace;
+};
+
+template <int DH>
+struct Shape {
+  static constexpr bool kTail = DH == 80;
+  static constexpr int MAIN = BQ * 128;
+  static constexpr int TILE = ((MAIN + (kTail ? BQ * 32 : 0) + 1023) / 1024) * 1024;
+};
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint4 scale_pack8(const uint32_t* v, float s) {
+  uint4 w;
+  w.x = pack_bf16(__uint_as_float(v[0]) * s, __uint_as_float(v[1]) * s);
+  w.y = pack_bf16(__uint_as_float(v[2]) * s, __uint_as_float(v[3]) * s);
+  w.z = pack_bf16(__uint_as_float(v[4]) * s, __uint_as_float(v[5]) * s);
+  w.w = pack_bf16(__uint_as_float(v[6]) * s, __uint_as_float(v[7]) * s);
+  return w;
+}
+// chunks of item with query tile i: 0..p-1, then the diagonal min(i, T-1) when it is >= p
+__device__ __forceinline__ int n_chunks(const Params& P, int i) {
+  const int d = min(i, P.T - 1);
+  return P.prefix + (d >= P.prefix ? 1 : 0);
+}
+__device__ __forceinline__ int chunk_of(const Params& P, int i, int j) { return j < P.prefix ? j : min(i, P.T - 1); }
+
+// [rows, 128] fp16: bh in columns [0, w), bw in [64, 64 + w), zeros elsewhere
+__global__ void glob_bias_prep_kernel(const float* __restrict__ bh, const float* __restrict__ bw, int rows, int w,
+                                      __half* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)rows * 128) return;
+  const long long r = i >> 7;
+  const int c = (int)(i & 127), j = c & 63;
+  float v = 0.f;
+  if (j < w) v = (c < 64 ? bh : bw)[r * w + j];
+  out[i] = __float2half_rn(v);
+}
+
+}  // namespace attng
+
+// Debug timeline (ZS_GLOB_TRACE=1): clock64() stamps of CTA 0's first items, 16 slots per item.
+__device__ unsigned long long g_glob_trace[64 * 16];
+#define ZG_TR(k, slot)                                                                       \
+  do {                                                                                       \
+    if (P.trace && blockIdx.x == 0 && (k) < 64) g_glob_trace[(k) * 16 + (slot)] = clock64(); \
+  } while (0)
+
+template <int DH>
+__global__ void __launch_bounds__(attng::kThreads, 1)
+    zs_attn_glob_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tq_t,
+                        const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tk_t,
+                        const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tv_t,
+                        const attng::Params P) {
+  using namespace attng;
+  using L = Shape<DH>;
+  constexpr bool kTail = L::kTail;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + P.off_bar);
+  uint64_t* q_full = bar + 0;       // [2]
+  uint64_t* q_empty = bar + 2;      // [2]
+  uint64_t* k_full = bar + 4;       // [KST]
+  uint64_t* k_empty = bar + 7;      // [KST]
+  uint64_t* v_full = bar + 10;      // [VST]
+  uint64_t* v_empty = bar + 12;     // [VST]
+  uint64_t* s_full = bar + 14;      // [wg]
+  uint64_t* p_full = bar + 16;      // [wg]  4 warps: P of the chunk in TMEM
+  uint64_t* o_full = bar + 18;      // [wg]  PV of the chunk completed
+  uint64_t* o_free = bar + 20;      // 8 warps: O_0 / O_1 read by the item's epilogue
+  uint64_t* m_full = bar + 21;      // [MST] key metadata of a chunk
+  uint64_t* m_empty = bar + 24;     // [MST] 4 warps of the consuming WG
+  uint64_t* b_full = bar + 27;      // [2] bias rows of the item staged (item parity)
+  uint64_t* b_empty = bar + 29;     // [2] 8 warps: item's last logits done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 32);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int2* koff = reinterpret_cast<int2*>(smem + P.off_koff);  // [MST][128]
+  // staged fp16 bias rows [2 item parity][128 rows][130 halves]: the 260-byte (65-word) row stride makes the
+  // per-key lookups of 32 consecutive rows bank-conflict free
+  uint8_t* bias_s = smem + P.off_bias;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tq);
+    tma_prefetch_desc(&tk);
+    tma_prefetch_desc(&tv);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 4);
+      mbar_init(&o_full[s], 1);
+    }
+    for (int s = 0; s < KST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < VST; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int s = 0; s < MST; ++s) {
+      mbar_init(&m_full[s], 1);
+      mbar_init(&m_empty[s], 4);
+    }
+    mbar_init(o_free, 8);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int nmb = P.T;  // query tiles per (unit, head)
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
+    if (warp == 0) {
+      // ---------------------------------------------------------- TMA producer
+      // lane 0: Q per item + K per chunk; lane 1: V per chunk (independent rings)
+      if (lane < 2) {
+        int k = 0, c = 0;
+        for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
+          const int i = it % nmb, uh = it / nmb, h = uh % P.heads, u = uh / P.heads, col = h * DH;
+          if (lane == 0) {
+            const int qs = k & 1;
+            mbar_wait_sleep(&q_empty[qs], ((k >> 1) & 1) ^ 1);
+            mbar_expect_tx(&q_full[qs], BQ * DH * 2);
+            uint8_t* q = smem + P.off_q + qs * L::TILE;
+            tma_load_3d(q, &tq, &q_full[qs], col, i * BQ, u);
+            if constexpr (kTail) tma_load_3d(q + L::MAIN, &tq_t, &q_full[qs], col + 64, i * BQ, u);
+          }
+          const int nc = n_chunks(P, i);
+          for (int j = 0; j < nc; ++j, ++c) {
+            const int cj = chunk_of(P, i, j);
+            if (lane == 0) {
+              const int s = c % KST;
+              mbar_wait_sleep(&k_empty[s], ((c / KST) & 1) ^ 1);
+              mbar_expect_tx(&k_full[s], BQ * DH * 2);
+              uint8_t* kk = smem + P.off_k + s * L::TILE;
+              tma_load_3d(kk, &tk, &k_full[s], col, cj * BQ, u);
+              if constexpr (kTail) tma_load_3d(kk + L::MAIN, &tk_t, &k_full[s], col + 64, cj * BQ, u);
+            } else {
+              const int s = c % VST;
+              mbar_wait_sleep(&v_empty[s], ((c / VST) & 1) ^ 1);
+              mbar_expect_tx(&v_full[s], BQ * DH * 2);
+              uint8_t* vv = smem + P.off_v + s * L::TILE;
+              tma_load_3d(vv, &tv, &v_full[s], col, cj * BQ, u);
+              if constexpr (kTail) tma_load_3d(vv + L::MAIN, &tv_t, &v_full[s], col + 64, cj * BQ, u);
+            }
+          }
+        }
+      }
+    } else if (warp == 1) {
+      // ---------------------------------------------------------- MMA issuer (whole warp)
+      constexpr uint32_t id_s = idesc_bf16(BQ, BQ);
+      constexpr uint32_t id_pv = idesc_bf16(BQ, 64, false, true);
+      constexpr uint32_t id_pv2 = idesc_bf16(BQ, 16, false, true);
+      constexpr uint32_t TILE16 = L::TILE >> 4;
+      const uint64_t dq = sdesc_k_sw128(smem + P.off_q), dqt = sdesc_k_sw32(smem + P.off_q + L::MAIN);
+      const uint64_t dk = sdesc_k_sw128(smem + P.off_k), dkt = sdesc_k_sw32(smem + P.off_k + L::MAIN);
+      const uint64_t dv = sdesc_mn_sw128(smem + P.off_v), dvt = sdesc_mn_sw32(smem + P.off_v + L::MAIN);
+      // S(c) of chunk ordinal c (item k, chunk j, WG w = j & 1)
+      auto issue_s = [&](int c, int k, int w, bool last) {
+        const int ks_ = c % KST, qs = k & 1;
+        mbar_wait(&k_full[ks_], (c / KST) & 1);
+        tc_fence_after();
+        const uint64_t q = dq + qs * TILE16, qt = dqt + qs * TILE16;
+        const uint64_t kk = dk + ks_ * TILE16, kt = dkt + ks_ * TILE16;
+        const uint32_t d = tmem + TM_S + w * 128;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) umma_ss(d, q + 2 * ks, kk + 2 * ks, id_s, ks > 0);
+        if constexpr (kTail) umma_ss(d, qt, kt, id_s, 1);
+        umma_commit_elect(&s_full[w]);
+        umma_commit_elect(&k_empty[ks_]);
+        if (last) umma_commit_elect(&q_empty[qs]);
+      };
+      auto issue_pv = [&](int c, int w, bool first) {
+        const int vs = c % VST;
+        mbar_wait(&v_full[vs], (c / VST) & 1);
+        tc_fence_after();
+        const uint64_t v = dv + vs * TILE16, vt = dvt + vs * TILE16;
+        const uint32_t a0 = tmem + TM_S + w * 128;
+        const uint32_t d = tmem + TM_O + w * 128;
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks) {
+          const uint32_t acc = (!first || ks > 0) ? 1u : 0u;
+          umma_ts(d, a0 + 8 * ks, v + ks * (16 * 128 / 16), id_pv, acc);
+          if constexpr (kTail) umma_ts(d + 64, a0 + 8 * ks, vt + ks * (16 * 32 / 16), id_pv2, acc);
+        }
+        umma_commit_elect(&o_full[w]);
+        umma_commit_elect(&v_empty[vs]);
+      };
+      // PV(c-1) is issued right after S(c): S(c) goes to the other WG's S buffer, and S(c)
+      // into S_w always follows PV(c-2) (same WG) in issue order, so P_w is read before it
+      // is overwritten (tcgen05.mma executes in order)
+      int npv[2] = {0, 0};
+      int pend_c = -1, pend_w = 0, pend_k = 0;
+      bool pend_first = false;
+      auto flush_pv = [&]() {
+        mbar_wait(&p_full[pend_w], npv[pend_w] & 1);
+        if (pend_first && pend_k > 0) mbar_wait(o_free, (pend_k - 1) & 1);  // previous epilogue read O
+        tc_fence_after();
+        issue_pv(pend_c, pend_w, pend_first);
+        npv[pend_w]++;
+      };
+      int k = 0, c = 0;
+      for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
+        const int i = it % nmb;
+        const int nc = n_chunks(P, i);
+        mbar_wait(&q_full[k & 1], (k >> 1) & 1);
+        if (lane == 0) ZG_TR(k, 6);
+        for (int j = 0; j < nc; ++j, ++c) {
+          const int w = c & 1;  // chunks alternate WGs across item boundaries too
+          issue_s(c, k, w, j == nc - 1);
+          if (lane == 0 && j < 6) ZG_TR(k, 7 + j);
+          if (pend_c >= 0) flush_pv();
+          pend_c = c;
+          pend_w = w;
+          pend_k = k;
+          pend_first = j < 2;  // first chunk of WG w in this item: O_w starts fresh
+        }
+      }
+      if (pend_c >= 0) flush_pv();
+    } else if (warp == 2) {
+      // ---------------------------------------------------------- key metadata per chunk
+      int c = 0;
+      for (int it = blockIdx.x; it < P.items; it += gridDim.x) {
+        const int i = it % nmb, u = it / nmb / P.heads;
+        const int nc = n_chunks(P, i);
+        for (int j = 0; j < nc; ++j, ++c) {
+          const int cj = chunk_of(P, i, j), s = c % MST;
+          int ksp[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int kg = cj * BQ + lane + 32 * q;
+            ksp[q] = kg < P.S ? __ldg(P.k_sp + (long long)u * P.S + kg) : -1;
+          }
+          mbar_wait_sleep(&m_empty[s], ((c / MST) & 1) ^ 1);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            koff[s * BQ + lane + 32 * q] =
+                ksp[q] >= 0 ? make_int2((ksp[q] / P.bias_w) * 2, (64 + ksp[q] % P.bias_w) * 2) : make_int2(0, 128);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&m_full[s]);
+        }
+      }
+    } else {
+      // ---------------------------------------------------------- bias rows of each item (warp 3)
+      // fp16 rows btab[h, σq(r)] (256 B) -> smem rows of 260 B; 16-byte loads (2 rows per
+      // instruction, 32 rows in flight), 4-byte stores.  Double-buffered by item parity.
+      int k = 0;
+      for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
+        const int i = it % nmb, uh = it / nmb, h = uh % P.heads, u = uh / P.heads;
+        const int bb = k & 1;
+        int qsp[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = i * BQ + lane + 32 * q;
+          qsp[q] = r < P.S ? __ldg(P.q_sp + (long long)u * P.S + r) : -1;
+        }
+        const __half* tab = P.btab + (long long)h * P.S * 128;
+        uint8_t* dst0 = bias_s + bb * (BQ * 260);
+        const int half = lane >> 4, ch = lane & 15;
+        mbar_wait_sleep(&b_empty[bb], ((k >> 1) & 1) ^ 1);
+        if (lane == 0) ZG_TR(k, 0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 v[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            const int sp = __shfl_sync(0xffffffffu, qsp[q], 2 * t + half);
+            v[t] = sp >= 0 ? __ldg(reinterpret_cast<const uint4*>(tab + (long long)sp * 128) + ch)
+                           : make_uint4(0u, 0u, 0u, 0u);
+          }
+#pragma unroll
+          for (int t = 0; t < 16; ++t) {
+            uint32_t* d = reinterpret_cast<uint32_t*>(dst0 + (32 * q + 2 * t + half) * 260 + ch * 16);
+            d[0] = v[t].x;
+            d[1] = v[t].y;
+            d[2] = v[t].z;
+            d[3] = v[t].w;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&b_full[bb]);
+          ZG_TR(k, 1);
+        }
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
+    // ------------------------------------------------------------ softmax warpgroups
+    const int w = (warp - 4) >> 2;  // WG: chunks j with j % 2 == w
+    const int wq = warp & 3;
+    const int r = wq * 32 + lane;   // row within the tile == TMEM lane
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const uint32_t s_addr = tmem + TM_S + w * 128 + lane_off;
+    const uint32_t o_addr = tmem + TM_O + w * 128 + lane_off;
+    const uint32_t o_oth = tmem + TM_O + (w ^ 1) * 128 + lane_off;
+    const uint8_t* brow0 = bias_s + r * 260;
+    float* ml = reinterpret_cast<float*>(smem + P.off_ml);  // [item parity][2 wg][2][BQ]: m, l
+    constexpr float L2E = 1.4426950408889634f;
+    constexpr float kThr = 5.545177444479562f;  // ln 256
+    const float tau = P.tau;
+    int k = 0, c = 0, nsw = 0;  // nsw: chunks this WG processed (phase of s_full / o_full)
+    (void)c;
+    for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
+      const int i = it % nmb, uh = it / nmb, h = uh % P.heads, u = uh / P.heads;
+      const int nc = n_chunks(P, i);
+      const int row = i * BQ + r;
+      mbar_wait(&b_full[k & 1], (k >> 1) & 1);
+      const char* bh_row = reinterpret_cast<const char*>(brow0 + (k & 1) * (BQ * 260));
+      if (lane == 0 && wq == 0) ZG_TR(k, 2 + w);
+      float m_ref = -INFINITY, ell = 0.f;
+      int mine = 0;  // chunks of this item processed by this WG
+      for (int j = 0; j < nc; ++j, ++c) {
+        if ((c & 1) != w) continue;
+        const int s = c % MST;
+        mbar_wait(&m_full[s], (c / MST) & 1);
+        const int2* ko = koff + s * BQ;
+        const int cj = chunk_of(P, i, j);
+        const int kvalid = P.S - cj * BQ;  // keys of this chunk below S
+        // bias of a 32-key group (independent of S: overlaps the S MMA / TMEM load latency)
+        auto group_bias = [&](int g, float (&b)[32]) {
+#pragma unroll
+          for (int jj = 0; jj < 32; jj += 2) {
+            const int4 oo = *reinterpret_cast<const int4*>(ko + 32 * g + jj);
+            b[jj] = __half2float(*reinterpret_cast<const __half*>(bh_row + oo.x)) +
+                    __half2float(*reinterpret_cast<const __half*>(bh_row + oo.y));
+            b[jj + 1] = __half2float(*reinterpret_cast<const __half*>(bh_row + oo.z)) +
+                        __half2float(*reinterpret_cast<const __half*>(bh_row + oo.w));
+          }
+        };
+        float bg[32];
+        group_bias(0, bg);
+        mbar_wait(&s_full[w], nsw & 1);
+        tc_fence_after();
+        uint32_t sr[128];
+        tmem_ld32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(sr));
+        float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          tmem_ld_wait();
+#pragma unroll
+          for (int jj = 0; jj < 32; jj += 2) {
+            const float x0 = fmaf(tau, __uint_as_float(sr[32 * g + jj]), bg[jj]);
+            const float x1 = fmaf(tau, __uint_as_float(sr[32 * g + jj + 1]), bg[jj + 1]);
+            sr[32 * g + jj] = __float_as_uint(x0);
+            sr[32 * g + jj + 1] = __float_as_uint(x1);
+            m0 = fmaxf(m0, x0);
+            m1 = fmaxf(m1, x1);
+          }
+          if (g < 3) {
+            tmem_ld32(s_addr + 32 * (g + 1), *reinterpret_cast<uint32_t(*)[32]>(sr + 32 * (g + 1)));
+            group_bias(g + 1, bg);
+          }
+        }
+        if (kvalid < BQ) {
+#pragma unroll
+          for (int jj = 0; jj < 128; ++jj)
+            if (jj >= kvalid) sr[jj] = __float_as_uint(-INFINITY);
+          m0 = -INFINITY;
+          m1 = -INFINITY;
+#pragma unroll
+          for (int jj = 0; jj < 128; jj += 2) {
+            m0 = fmaxf(m0, __uint_as_float(sr[jj]));
+            m1 = fmaxf(m1, __uint_as_float(sr[jj + 1]));
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&m_empty[s]);
+        if (j >= nc - 2) {  // this WG's last chunk of the item: bias rows no longer needed
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&b_empty[k & 1]);
+        }
+        const float mx = fmaxf(m0, m1);
+        // lazy rescale: the reference max moves only past the threshold
+        float alpha = 1.f;
+        if (mx > m_ref + kThr || (m_ref == -INFINITY && mx > -INFINITY)) {
+          alpha = (m_ref == -INFINITY) ? 0.f : ex2((m_ref - mx) * L2E);
+          if (mine > 0) {
+            // previous PV into O_w must have completed before O_w is rescaled
+            mbar_wait(&o_full[w], (nsw - 1) & 1);
+            tc_fence_after();
+            uint32_t pr[32];
+            tmem_ld32(o_addr, pr);
+            tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 32; ++q) pr[q] = __float_as_uint(__uint_as_float(pr[q]) * alpha);
+            tmem_st32(o_addr, pr);
+            tmem_ld32(o_addr + 32, pr);
+            tmem_ld_wait();
+#pragma unroll
+            for (int q = 0; q < 32; ++q) pr[q] = __float_as_uint(__uint_as_float(pr[q]) * alpha);
+            tmem_st32(o_addr + 32, pr);
+            if constexpr (DH == 80) {
+              uint32_t p16[16];
+              tmem_ld16(o_addr + 64, p16);
+              tmem_ld_wait();
+#pragma unroll
+              for (int q = 0; q < 16; ++q) p16[q] = __float_as_uint(__uint_as_float(p16[q]) * alpha);
+              tmem_st16(o_addr + 64, p16);
+            }
+          }
+          m_ref = mx;
+        }
+        const float mc = (m_ref == -INFINITY) ? 0.f : m_ref * L2E;
+        float r0 = 0.f, r1 = 0.f;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float a = ex2(fmaf(__uint_as_float(sr[32 * g + 2 * q]), L2E, -mc));
+            const float b = ex2(fmaf(__uint_as_float(sr[32 * g + 2 * q + 1]), L2E, -mc));
+            r0 += a;
+            r1 += b;
+            pk[q] = pack_bf16(a, b);
+          }
+          tmem_st16(s_addr + 16 * g, pk);
+        }
+        ell = ell * alpha + (r0 + r1);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[w]);
+        ++nsw;
+        ++mine;
+      }
+      if (mine == 0) {  // no chunk of this item for this WG (nc == 1)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&b_empty[k & 1]);
+      }
+      // ---- item epilogue: merge the two WGs' partial softmaxes, each WG writes half the columns
+      float* mlk = ml + (k & 1) * 4 * BQ;
+      mlk[(w * 2 + 0) * BQ + r] = m_ref;
+      mlk[(w * 2 + 1) * BQ + r] = ell;
+      // wait for this WG's last PV and the other WG's (its m / l are posted before the barrier)
+      if (mine > 0) mbar_wait(&o_full[w], (nsw - 1) & 1);
+      named_bar_sync(1, 256);
+      const float mo = mlk[((w ^ 1) * 2 + 0) * BQ + r], lo = mlk[((w ^ 1) * 2 + 1) * BQ + r];
+      // the other WG's last PV: it waited for it before the barrier
+      const float mm = fmaxf(m_ref, mo);
+      const float a_me = (m_ref == -INFINITY) ? 0.f : ex2((m_ref - mm) * L2E);
+      const float a_ot = (mo == -INFINITY) ? 0.f : ex2((mo - mm) * L2E);
+      const float inv = 1.0f / (ell * a_me + lo * a_ot);
+      const float s_me = a_me * inv, s_ot = a_ot * inv;
+      tc_fence_after();
+      const bool valid = row < P.S;
+      __nv_bfloat16* dst = P.out + (long long)u * P.o_unit_stride + (long long)row * P.ldo + h * DH;
+      // WG0: columns [0, 32) (+ [64, 80) when dh = 80), WG1: [32, 64)
+      {
+        const uint32_t c0 = w * 32;
+        uint32_t a[32], b[32];
+        tmem_ld32(o_addr + c0, a);
+        tmem_ld32(o_oth + c0, b);
+        tmem_ld_wait();
+        if (valid) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e)  // a WG without chunks has a stale O: weight exactly 0
+              v[e] = __float_as_uint((s_me != 0.f ? __uint_as_float(a[8 * q + e]) * s_me : 0.f) +
+                                     (s_ot != 0.f ? __uint_as_float(b[8 * q + e]) * s_ot : 0.f));
+            d4[q] = scale_pack8(v, 1.f);
+          }
+        }
+      }
+      if constexpr (DH == 80) {
+        if (w == 0) {
+          uint32_t a[16], b[16];
+          tmem_ld16(o_addr + 64, a);
+          tmem_ld16(o_oth + 64, b);
+          tmem_ld_wait();
+          if (valid) {
+            uint32_t v[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              v[e] = __float_as_uint((s_me != 0.f ? __uint_as_float(a[e]) * s_me : 0.f) +
+                                     (s_ot != 0.f ? __uint_as_float(b[e]) * s_ot : 0.f));
+            uint4* d4 = reinterpret_cast<uint4*>(dst + 64);
+            d4[0] = scale_pack8(v, 1.f);
+            d4[1] = scale_pack8(v + 8, 1.f);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(o_free);
+      if (lane == 0 && wq == 0) ZG_TR(k, 4 + w);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem, kTmemCols);
+}
+
+}  // namespace zs
+
+using namespace zs;
+
+// Host launcher: returns 1 when outside this kernel's envelope (b_row = b_col = 128, square
+// grids, dh 64 / 80), 0 on launch, negative on error.
+int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
+                     long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
+                     const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
+                     float tau, void* out, long long ldo, long long ous, cudaStream_t st) {
+  using namespace attng;
+  if (b_row != BQ || b_col != BQ || (dh != 64 && dh != 80) || S < 1 || bias_w > 64) return 1;
+  Params p{};
+  p.units = units;
+  p.heads = heads;
+  p.S = S;
+  p.bias_w = bias_w;
+  p.W1 = 130;
+  p.T = (S + BQ - 1) / BQ;
+  p.prefix = prefix;
+  const long long items = (long long)units * heads * p.T;
+  if (items > 0x7FFFFFFF) return ZS_ERR_SHAPE;
+  p.items = (int)items;
+  p.ldo = ldo;
+  p.o_unit_stride = ous;
+  p.q_sp = q_sp;
+  p.k_sp = k_sp;
+  p.tau = tau;
+  p.out = reinterpret_cast<__nv_bfloat16*>(out);
+  p.trace = getenv("ZS_GLOB_TRACE") ? 1 : 0;
+  const int tile = dh == 80 ? Shape<80>::TILE : Shape<64>::TILE;
+  p.tile = tile;
+  int off = 0;
+  auto take = [&](int bytes, int align) {
+    off = (off + align - 1) / align * align;
+    const int o = off;
+    off += bytes;
+    return o;
+  };
+  p.off_q = take(2 * tile, 1024);
+  p.off_k = take(KST * tile, 1024);
+  p.off_v = take(VST * tile, 1024);
+  p.off_bias = take(2 * BQ * 260, 16);
+  p.off_koff = take(MST * BQ * 8, 16);
+  p.off_ml = take(2 * 4 * BQ * 4, 16);
+  p.off_bar = take(512, 8);
+  const size_t smem = 1024 + (size_t)off;
+  if (smem > 227 * 1024) return 1;
+  // fp16 bias rows [heads, S, 128] (scratch, grow-only per device)
+  {
+    static __half* buf[64] = {nullptr};
+    static size_t cap[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return ZS_ERR_DEVICE;
+    const size_t need = (size_t)heads * S * 128;
+    if (cap[dev] < need) {
+      if (buf[dev]) cudaFree(buf[dev]);
+      buf[dev] = nullptr;
+      cap[dev] = 0;
+      if (cudaMalloc(&buf[dev], need * sizeof(__half)) != cudaSuccess) return ZS_ERR_DEVICE;
+      cap[dev] = need;
+    }
+    const long long n = (long long)need;
+    glob_bias_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(bh, bw, heads * S, bias_w, buf[dev]);
+    p.btab = buf[dev];
+  }
+  CUtensorMap m[6];
+  const uint64_t ncol = (uint64_t)heads * dh;
+  int rc = 0;
+  rc |= make_tmap_3d_bf16(&m[0], q, ncol, S, units, ldq, qus, 64, BQ, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+  rc |= make_tmap_3d_bf16(&m[2], k, ncol, S, units, ldk, kvus, 64, BQ, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+  rc |= make_tmap_3d_bf16(&m[4], v, ncol, S, units, ldv, kvus, 64, BQ, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (dh == 80) {
+    rc |= make_tmap_3d_bf16(&m[1], q, ncol, S, units, ldq, qus, 16, BQ, 1, CU_TENSOR_MAP_SWIZZLE_32B);
+    rc |= make_tmap_3d_bf16(&m[3], k, ncol, S, units, ldk, kvus, 16, BQ, 1, CU_TENSOR_MAP_SWIZZLE_32B);
+    rc |= make_tmap_3d_bf16(&m[5], v, ncol, S, units, ldv, kvus, 16, BQ, 1, CU_TENSOR_MAP_SWIZZLE_32B);
+  } else {
+    m[1] = m[0];
+    m[3] = m[2];
+    m[5] = m[4];
+  }
+  if (rc) return ZS_ERR_TMAP;
+  int grid = num_sms();
+  if (grid > p.items) grid = p.items;
+  if (dh == 64) {
+    cudaFuncSetAttribute(zs_attn_glob_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    zs_attn_glob_kernel<64><<<grid, kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p);
+  } else {
+    cudaFuncSetAttribute(zs_attn_glob_kernel<80>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    zs_attn_glob_kernel<80><<<grid, kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
+}
+
+extern "C" __attribute__((visibility("default"))) int zs_debug_glob_trace(unsigned long long* host, int n) {
+  if (n > 64 * 16) n = 64 * 16;
+  return cudaMemcpyFromSymbol(host, g_glob_trace, n * sizeof(unsigned long long)) == cudaSuccess ? 0 : -1;
+}

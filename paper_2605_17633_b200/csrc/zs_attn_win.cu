@@ -252,9 +252,9 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   // register budget: the single-lane producer / MMA / operand warpgroup gives registers to the
-  // softmax warpgroups, whose rows live in registers (128*80 + 256*208 <= 384*168 at launch)
+  // softmax warpgroups, whose rows live in registers (128*96 + 256*200 <= 384*168 at launch)
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
     if (warp == 0) {
       // ---------------------------------------------------------- TMA producer
       if (lane == 0) {
@@ -291,37 +291,36 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         }
       }
     } else if (warp == 1) {
-      // ---------------------------------------------------------- MMA issuer (one lane)
+      // ---------------------------------------------------------- MMA issuer (whole warp, elected lane)
       constexpr uint32_t id_pv = idesc_bf16(128, 64, false, true);
       constexpr uint32_t id_pv2 = idesc_bf16(128, 16, false, true);
+      // descriptors of buffer 0 hoisted; buffer b / row offsets are added in 16-byte units
+      const uint32_t bufd = (uint32_t)P.buf_bytes >> 4;
+      const uint64_t dq[2] = {sdesc_k_sw128(smem + P.off_qa), sdesc_k_sw128(smem + P.off_qb)};
+      const uint64_t dqt[2] = {sdesc_k_sw32(smem + P.off_qa_t), sdesc_k_sw32(smem + P.off_qb_t)};
+      const uint64_t dk = sdesc_k_sw128(smem + P.off_k), dkt = sdesc_k_sw32(smem + P.off_k_t);
+      const uint64_t dbh = sdesc_k_sw32(smem + P.off_bq_h), dbw = sdesc_k_sw32(smem + P.off_bq_w);
+      const uint64_t dkh = sdesc_k_sw32(smem + P.off_kb_h), dkw = sdesc_k_sw32(smem + P.off_kb_w);
+      const uint64_t dv = sdesc_mn_sw128(smem + P.off_v), dvt = sdesc_mn_sw32(smem + P.off_v_t);
       auto issue_s = [&](int X, int b) {
-        uint8_t* base = smem + b * P.buf_bytes;
-        uint8_t* q = base + (X ? P.off_qb : P.off_qa);
-        uint8_t* qt = base + (X ? P.off_qb_t : P.off_qa_t);
-        uint8_t* kk = base + P.off_k;
-        uint8_t* kt = base + P.off_k_t;
-        uint8_t* bqh = smem + P.off_bq_h + X * 128 * 32;
-        uint8_t* bqw = smem + P.off_bq_w + X * 128 * 32;
-        uint8_t* kbh = smem + P.off_kb_h;
-        uint8_t* kbw = smem + P.off_kb_w;
+        const uint64_t q = dq[X] + b * bufd, qt = dqt[X] + b * bufd;
+        const uint64_t kk = dk + b * bufd, kt = dkt + b * bufd;
+        const uint64_t bh = dbh + X * 256, bw = dbw + X * 256;  // tile B rows start at row 128 (x32 B)
         const uint32_t d0 = tmem + P.s_col[X];
         for (int r = 0; r < P.nrun[X]; ++r) {
           const int k0 = P.run_k0[X][r], n = P.run_n[X][r];
           const uint32_t id = idesc_bf16(128, n), idh = idesc_f16(128, n);
           const uint32_t d = d0 + P.run_c0[X][r];
 #pragma unroll
-          for (int ks = 0; ks < 4; ++ks)
-            umma_bf16(d, sdesc_k_sw128(q) + 2 * ks, sdesc_k_sw128(kk + k0 * 128) + 2 * ks, id, ks > 0);
-          if constexpr (kTail) umma_bf16(d, sdesc_k_sw32(qt), sdesc_k_sw32(kt + k0 * 32), id, 1);
-          umma_bf16(d, sdesc_k_sw32(bqh), sdesc_k_sw32(kbh + k0 * 32), idh, 1);  // + bh[σq, ky] / tau
-          umma_bf16(d, sdesc_k_sw32(bqw), sdesc_k_sw32(kbw + k0 * 32), idh, 1);  // + bw[σq, kx] / tau
+          for (int ks = 0; ks < 4; ++ks) umma_ss(d, q + 2 * ks, kk + k0 * 8 + 2 * ks, id, ks > 0);
+          if constexpr (kTail) umma_ss(d, qt, kt + k0 * 2, id, 1);
+          umma_ss(d, bh, dkh + k0 * 2, idh, 1);  // + bh[σq, ky] / tau
+          umma_ss(d, bw, dkw + k0 * 2, idh, 1);  // + bw[σq, kx] / tau
         }
-        umma_commit(&s_full[X]);
+        umma_commit_elect(&s_full[X]);
       };
       auto issue_pv = [&](int X, int b) {
-        uint8_t* base = smem + b * P.buf_bytes;
-        uint8_t* vv = base + P.off_v;
-        uint8_t* vt = base + P.off_v_t;
+        const uint64_t vv = dv + b * bufd, vt = dvt + b * bufd;
         const uint32_t a0 = tmem + P.s_col[X];
         const uint32_t d = tmem + P.o_col[X];
         uint32_t acc = 0;
@@ -330,51 +329,48 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
           for (int s = 0; s < n / 16; ++s) {
             const uint32_t a = a0 + (uint32_t)((c0 >> 1) + 8 * s);
             const int kr = k0 + 16 * s;
-            umma_bf16_ts(d, a, sdesc_mn_sw128(vv + kr * 128), id_pv, acc);
-            if constexpr (kTail) umma_bf16_ts(d + 64, a, sdesc_mn_sw32(vt + kr * 32), id_pv2, acc);
+            umma_ts(d, a, vv + kr * 8, id_pv, acc);
+            if constexpr (kTail) umma_ts(d + 64, a, vt + kr * 2, id_pv2, acc);
             acc = 1;
           }
         }
-        umma_commit(&o_full[X]);
+        umma_commit_elect(&o_full[X]);
       };
-      if (lane == 0) {
-        int k = 0, pb = 0;
-        for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
-          const int b = k & 1;
-          mbar_wait(&qk_full[b], (k >> 1) & 1);
-          mbar_wait(bk_full, k & 1);
-          tc_fence_after();
-          issue_s(0, b);
-          ZS_TR(k, 2);
-          if (nt > 1) {
-            if (k > 0) {  // PV of tile B, previous item
-              mbar_wait(&p_full[1], (k - 1) & 1);
-              tc_fence_after();
-              issue_pv(1, pb);
-              umma_commit(&v_empty[pb]);
-              ZS_TR(k, 3);
-            }
-            issue_s(1, b);
-            ZS_TR(k, 4);
+      int k = 0, pb = 0;
+      for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
+        const int b = k & 1;
+        mbar_wait(&qk_full[b], (k >> 1) & 1);
+        mbar_wait(bk_full, k & 1);
+        tc_fence_after();
+        issue_s(0, b);
+        if (lane == 0) ZS_TR(k, 2);
+        if (nt > 1) {
+          if (k > 0) {  // PV of tile B, previous item
+            mbar_wait(&p_full[1], (k - 1) & 1);
+            tc_fence_after();
+            issue_pv(1, pb);
+            umma_commit_elect(&v_empty[pb]);
+            if (lane == 0) ZS_TR(k, 3);
           }
-          umma_commit(&qk_empty[b]);
-          umma_commit(bk_empty);
-          mbar_wait(&p_full[0], k & 1);
-          mbar_wait(&v_full[b], (k >> 1) & 1);
-          tc_fence_after();
-          issue_pv(0, b);
-          ZS_TR(k, 5);
-          if (nt == 1) umma_commit(&v_empty[b]);
-          pb = b;
+          issue_s(1, b);
+          if (lane == 0) ZS_TR(k, 4);
         }
-        if (nt > 1 && k > 0) {
-          mbar_wait(&p_full[1], (k - 1) & 1);
-          tc_fence_after();
-          issue_pv(1, pb);
-          umma_commit(&v_empty[pb]);
-        }
+        umma_commit_elect(&qk_empty[b]);
+        umma_commit_elect(bk_empty);
+        mbar_wait(&p_full[0], k & 1);
+        mbar_wait(&v_full[b], (k >> 1) & 1);
+        tc_fence_after();
+        issue_pv(0, b);
+        if (lane == 0) ZS_TR(k, 5);
+        if (nt == 1) umma_commit_elect(&v_empty[b]);
+        pb = b;
       }
-      __syncwarp();
+      if (nt > 1 && k > 0) {
+        mbar_wait(&p_full[1], (k - 1) & 1);
+        tc_fence_after();
+        issue_pv(1, pb);
+        umma_commit_elect(&v_empty[pb]);
+      }
     } else {
       // ---------------------------------------------------------- bias operands of each item
       //  warp 3 - Bq: fp16 rows btab[h, σq(r)] (two 16-column SW32 slabs bh | bw)
@@ -422,7 +418,7 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
       }
     }
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
     // ------------------------------------------------------------ softmax, one thread per row
     const int X = (warp - 4) >> 2;
     const int wq = warp & 3;
