@@ -76,6 +76,25 @@ __device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, 
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+__device__ __forceinline__ void umma_pair_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 rx;\n\t"
+      "elect.sync rx|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b32 rx;\n\t"
+      "elect.sync rx|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
 // commit this thread's MMAs to the barrier at the same offset in both CTAs of the pair
 __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
   asm volatile(
@@ -165,29 +184,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
     }
   } else if (warp == 1) {
     if (leader) {
+      // whole warp runs the loop (uniform registers, hoisted descriptors), one elected lane
+      // issues: rebuilding descriptors per MMA in a lane-0 branch costs ~120+ cycles per
+      // instruction (tools/mma_bench.cu), as much as a 256x256x16 MMA pair itself
       constexpr uint32_t idesc = idesc_bf16(2 * BM, BN);
+      const uint64_t da0 = sdesc_k_sw128(smem), db0 = sdesc_k_sw128(smem + A_BYTES);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
       for (int t = cid; t < num_tiles; t += ncl, ++it) {
         const int as = it & 1;
-        mbar_wait_sleep(&tempty[as], ((it >> 1) & 1) ^ 1);
+        mbar_wait(&tempty[as], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t dtm = tmem_base + as * BN;
         for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait_sleep(&full[stage], phase);
+          mbar_wait(&full[stage], phase);
           tc_fence_after();
-          if (lane == 0) {
-            uint8_t* sa = smem + stage * STAGE_BYTES;
-            uint8_t* sb = sa + A_BYTES;
-            const uint64_t da = sdesc_k_sw128(sa);
-            const uint64_t db = sdesc_k_sw128(sb);
+          const uint64_t da = da0 + (uint64_t)(stage * (STAGE_BYTES >> 4));
+          const uint64_t db = db0 + (uint64_t)(stage * (STAGE_BYTES >> 4));
 #pragma unroll
-            for (int k = 0; k < BK / UK; ++k) umma_bf16_pair(dtm, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
-            umma_commit_pair(&empty[stage]);
-            if (kb == nk - 1) umma_commit_pair(&tfull[as]);
-          }
-          __syncwarp();
+          for (int k = 0; k < BK / UK; ++k) umma_pair_elect(dtm, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+          umma_commit_pair_elect(&empty[stage]);
+          if (kb == nk - 1) umma_commit_pair_elect(&tfull[as]);
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
