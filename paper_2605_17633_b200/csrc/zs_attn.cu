@@ -233,7 +233,8 @@ __global__ void __launch_bounds__(attn::kThreads, 1)
   uint64_t* b_empty = bar + 26;     // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 28);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index via shfl: provably warp-uniform, so role code can use uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tq);

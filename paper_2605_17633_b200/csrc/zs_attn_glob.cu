@@ -7,25 +7,24 @@
 // except keys / rows past S.
 //
 // B200 design (one persistent CTA per SM):
+//  * Decomposed rel-pos bias on the tensor core: S' = q.k + Bq . OH^T, where Bq[r] =
+//    [bh[σq(r)] | bw[σq(r)]] / tau (fp16, 128 columns, resident in TMEM for the item and used
+//    as the A operand) and OH[k] = [e_{σk/64} | e_{σk%64}] (fp16 one-hot rows of the chunk's
+//    keys, generated in shared memory).  logit = tau * S', so the softmax does no gathers.
 //  * Two softmax warpgroups split the chunks (WG w takes the CTA's chunk ordinals c with
-//    c % 2 == w, so S(c) always targets the other WG's S buffer than S(c-1)), each
-//    with its own S buffer, O accumulator (TMEM) and running max / sum, so the two chunks'
-//    softmaxes run concurrently with no per-chunk exchange; the partial results merge once per
-//    item in the epilogue (each WG writes half of the output columns).
-//  * One thread per query row holds the 128 logits of a chunk in registers; the decomposed
-//    rel-pos bias bh[σq(r), σk/64] + bw[σq(r), σk%64] is looked up in an odd-stride fp32 row
-//    table (bank-conflict-free) staged per item by a dedicated warp with cp.async.
+//    c % 2 == w, so S(c) always targets the other WG's S buffer than S(c-1)), each with its
+//    own S buffer, O accumulator and running max / sum; the partial results merge once per
+//    item (each WG writes half of the output columns).
 //  * P (bf16) overwrites the WG's S columns in TMEM and is the A operand of the PV MMA.
 //  * Lazy rescaling: O_w is rescaled in TMEM only when the row max grows by more than ln 256.
-//  * MMA issue order S(0) S(1) PV(0) S(2) PV(1) ... keeps the tensor core busy on one WG's
-//    chunk while the other WG's softmax runs.
-// Roles: warp 0 TMA (Q per item, K / V ring per chunk), warp 1 MMA (whole warp, elected lane),
-// warp 2 TMEM owner + key metadata (σk -> bias byte offsets per chunk), warp 3 bias rows,
-// warps 4-7 WG0, warps 8-11 WG1.
+//  * The next item's Bq rows are prefetched with cp.async while the current item runs and
+//    written into TMEM (tcgen05.st) once its last S' MMA has completed.
+// Roles: warp 0 TMA (lane 0: Q per item + K per chunk, lane 1: V per chunk), warp 1 MMA (whole
+// warp, elected lane), warps 2-3 one-hot key rows per chunk, warps 4-7 WG0, warps 8-11 WG1.
+#include <cuda_fp16.h>
+
 #include <algorithm>
 #include <cstdlib>
-
-#include <cuda_fp16.h>
 
 #include "zs_common.cuh"
 #include "zs_host.h"
@@ -36,21 +35,24 @@ namespace attng {
 constexpr int BQ = 128;
 constexpr int kThreads = 384;
 constexpr uint32_t kTmemCols = 512;
-constexpr int KST = 3;  // K ring stages
-constexpr int VST = 2;  // V ring stages
-constexpr int MST = 3;  // key-metadata ring stages
-constexpr uint32_t TM_S = 0;    // S_w at [w*128, w*128+128)
-constexpr uint32_t TM_O = 256;  // O_w at 256 + w*128
+constexpr int KST = 2;  // K + one-hot ring stages
+constexpr int QST = 1;  // Q slots (the next item's Q loads once the last S' of the item completed)
+constexpr int VST = 3;  // V ring stages
+constexpr uint32_t TM_S = 0;     // S_w at [w*128, w*128+128)
+constexpr uint32_t TM_O = 256;   // O_w at 256 + w*80
+constexpr uint32_t TM_BQ = 416;  // Bq: 128 fp16 = 64 columns
+constexpr int OH_BYTES = 2 * BQ * 128;  // two 64-column SW128 slabs (e_ky | e_kx)
+constexpr int BQ_STRIDE = 272;          // bytes per staged Bq row (256 + 16 pad)
 
 struct Params {
-  int units, heads, S, bias_w, W1, T, prefix, items;
+  int units, heads, S, bias_w, T, prefix, items;
   long long ldo, o_unit_stride;
-  const __half* btab;  // [heads, S, 128] fp16 bias rows: bh in cols [0, w), bw in [64, 64 + w)
+  const __half* btab;  // [heads, S, 128] fp16 rows: bh/tau in cols [0, w), bw/tau in [64, 64 + w)
   const int* q_sp;
   const int* k_sp;
   float tau;
   __nv_bfloat16* out;
-  int off_q, off_k, off_v, off_bias, off_koff, off_ml, off_bar, tile;
+  int off_q, off_k, off_oh, off_v, off_bq, off_ml, off_bar, tile;
   int trace;
 };
 
@@ -61,13 +63,23 @@ struct Shape {
   static constexpr int TILE = ((MAIN + (kTail ? BQ * 32 : 0) + 1023) / 1024) * 1024;
 };
 
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+// two exponentials with one MUFU op: 2^a, 2^b through ex2.approx.f16x2.  The arguments are
+// <= ~8 (lazy max), so the fp16 rounding of the argument costs <= 0.14% relative on the terms
+// that matter, below the bf16 rounding of P that follows.
+__device__ __forceinline__ void ex2x2(float a, float b, float& ea, float& eb) {
+  uint32_t h;
+  asm("{\n\t.reg .b32 t;\n\tcvt.rn.f16x2.f32 t, %2, %1;\n\tex2.approx.f16x2 %0, t;\n\t}" : "=r"(h) : "f"(a), "f"(b));
+  __half2 hh = *reinterpret_cast<__half2*>(&h);
+  ea = __low2float(hh);
+  eb = __high2float(hh);
 }
 __device__ __forceinline__ uint4 scale_pack8(const uint32_t* v, float s) {
   uint4 w;
@@ -77,6 +89,10 @@ __device__ __forceinline__ uint4 scale_pack8(const uint32_t* v, float s) {
   w.w = pack_bf16(__uint_as_float(v[6]) * s, __uint_as_float(v[7]) * s);
   return w;
 }
+// fp16 x fp16 -> fp32 instruction descriptor (A/B K-major)
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
 // chunks of item with query tile i: 0..p-1, then the diagonal min(i, T-1) when it is >= p
 __device__ __forceinline__ int n_chunks(const Params& P, int i) {
   const int d = min(i, P.T - 1);
@@ -84,15 +100,15 @@ __device__ __forceinline__ int n_chunks(const Params& P, int i) {
 }
 __device__ __forceinline__ int chunk_of(const Params& P, int i, int j) { return j < P.prefix ? j : min(i, P.T - 1); }
 
-// [rows, 128] fp16: bh in columns [0, w), bw in [64, 64 + w), zeros elsewhere
+// [rows, 128] fp16 bias operand rows: bh/tau in columns [0, w), bw/tau in [64, 64 + w), zeros elsewhere
 __global__ void glob_bias_prep_kernel(const float* __restrict__ bh, const float* __restrict__ bw, int rows, int w,
-                                      __half* __restrict__ out) {
+                                      float inv_tau, __half* __restrict__ out) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (long long)rows * 128) return;
   const long long r = i >> 7;
   const int c = (int)(i & 127), j = c & 63;
   float v = 0.f;
-  if (j < w) v = (c < 64 ? bh : bw)[r * w + j];
+  if (j < w) v = (c < 64 ? bh : bw)[r * w + j] * inv_tau;
   out[i] = __float2half_rn(v);
 }
 
@@ -117,35 +133,34 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + P.off_bar);
-  uint64_t* q_full = bar + 0;       // [2]
-  uint64_t* q_empty = bar + 2;      // [2]
-  uint64_t* k_full = bar + 4;       // [KST]
-  uint64_t* k_empty = bar + 7;      // [KST]
-  uint64_t* v_full = bar + 10;      // [VST]
-  uint64_t* v_empty = bar + 12;     // [VST]
-  uint64_t* s_full = bar + 14;      // [wg]
-  uint64_t* p_full = bar + 16;      // [wg]  4 warps: P of the chunk in TMEM
-  uint64_t* o_full = bar + 18;      // [wg]  PV of the chunk completed
-  uint64_t* o_free = bar + 20;      // 8 warps: O_0 / O_1 read by the item's epilogue
-  uint64_t* m_full = bar + 21;      // [MST] key metadata of a chunk
-  uint64_t* m_empty = bar + 24;     // [MST] 4 warps of the consuming WG
-  uint64_t* b_full = bar + 27;      // [2] bias rows of the item staged (item parity)
-  uint64_t* b_empty = bar + 29;     // [2] 8 warps: item's last logits done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 32);
+  uint64_t* q_full = bar + 0;    // [QST]
+  uint64_t* q_empty = bar + 2;   // [QST]
+  uint64_t* k_full = bar + 4;    // [KST] K tile landed (TMA)
+  uint64_t* k_empty = bar + 8;   // [KST] S' of the chunk done: K and one-hot stage free
+  uint64_t* oh_full = bar + 12;  // [KST] one-hot rows written (warps 2, 3)
+  uint64_t* v_full = bar + 16;   // [VST]
+  uint64_t* v_empty = bar + 20;  // [VST]
+  uint64_t* s_full = bar + 24;   // [wg]
+  uint64_t* p_full = bar + 26;   // [wg]  4 warps: P of the chunk in TMEM
+  uint64_t* o_full = bar + 28;   // [wg]  PV of the chunk completed
+  uint64_t* o_free = bar + 30;   // 8 warps: O_0 / O_1 read by the item's epilogue
+  uint64_t* bq_full = bar + 31;  // 8 warps: the item's Bq rows are in TMEM
+  uint64_t* bq_free = bar + 32;  // the item's last S' completed (Bq may be replaced)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 34);
+  static_assert(KST <= 4 && VST <= 4 && QST <= 2, "barrier slots");
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int2* koff = reinterpret_cast<int2*>(smem + P.off_koff);  // [MST][128]
-  // staged fp16 bias rows [2 item parity][128 rows][130 halves]: the 260-byte (65-word) row stride makes the
-  // per-key lookups of 32 consecutive rows bank-conflict free
-  uint8_t* bias_s = smem + P.off_bias;
+  // warp index via shfl: provably warp-uniform, so role code can use uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tq);
     tma_prefetch_desc(&tk);
     tma_prefetch_desc(&tv);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < QST; ++s) {
       mbar_init(&q_full[s], 1);
       mbar_init(&q_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&p_full[s], 4);
       mbar_init(&o_full[s], 1);
@@ -153,20 +168,15 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     for (int s = 0; s < KST; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
+      mbar_init(&oh_full[s], 2);
     }
     for (int s = 0; s < VST; ++s) {
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
-    for (int s = 0; s < MST; ++s) {
-      mbar_init(&m_full[s], 1);
-      mbar_init(&m_empty[s], 4);
-    }
     mbar_init(o_free, 8);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&b_full[s], 1);
-      mbar_init(&b_empty[s], 8);
-    }
+    mbar_init(bq_full, 8);
+    mbar_init(bq_free, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
@@ -180,14 +190,13 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
     if (warp == 0) {
       // ---------------------------------------------------------- TMA producer
-      // lane 0: Q per item + K per chunk; lane 1: V per chunk (independent rings)
       if (lane < 2) {
         int k = 0, c = 0;
         for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
           const int i = it % nmb, uh = it / nmb, h = uh % P.heads, u = uh / P.heads, col = h * DH;
           if (lane == 0) {
-            const int qs = k & 1;
-            mbar_wait_sleep(&q_empty[qs], ((k >> 1) & 1) ^ 1);
+            const int qs = k % QST;
+            mbar_wait_sleep(&q_empty[qs], ((k / QST) & 1) ^ 1);
             mbar_expect_tx(&q_full[qs], BQ * DH * 2);
             uint8_t* q = smem + P.off_q + qs * L::TILE;
             tma_load_3d(q, &tq, &q_full[qs], col, i * BQ, u);
@@ -217,26 +226,39 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     } else if (warp == 1) {
       // ---------------------------------------------------------- MMA issuer (whole warp)
       constexpr uint32_t id_s = idesc_bf16(BQ, BQ);
+      constexpr uint32_t id_b = idesc_f16(BQ, BQ);
       constexpr uint32_t id_pv = idesc_bf16(BQ, 64, false, true);
       constexpr uint32_t id_pv2 = idesc_bf16(BQ, 16, false, true);
       constexpr uint32_t TILE16 = L::TILE >> 4;
       const uint64_t dq = sdesc_k_sw128(smem + P.off_q), dqt = sdesc_k_sw32(smem + P.off_q + L::MAIN);
       const uint64_t dk = sdesc_k_sw128(smem + P.off_k), dkt = sdesc_k_sw32(smem + P.off_k + L::MAIN);
+      const uint64_t doh = sdesc_k_sw128(smem + P.off_oh);
       const uint64_t dv = sdesc_mn_sw128(smem + P.off_v), dvt = sdesc_mn_sw32(smem + P.off_v + L::MAIN);
-      // S(c) of chunk ordinal c (item k, chunk j, WG w = j & 1)
+      // S'(c) of chunk ordinal c into S_w: q.k (bf16) then + Bq . OH^T (fp16, A from TMEM)
+      int first_c = 0;  // chunk ordinal of the current item's first chunk (trace only)
       auto issue_s = [&](int c, int k, int w, bool last) {
-        const int ks_ = c % KST, qs = k & 1;
+        const int ks_ = c % KST, qs = k % QST;
         mbar_wait(&k_full[ks_], (c / KST) & 1);
+        if (lane == 0 && c == first_c + 1) ZG_TR(k, 13);
+        mbar_wait(&oh_full[ks_], (c / KST) & 1);
+        if (lane == 0 && c == first_c + 1) ZG_TR(k, 14);
         tc_fence_after();
         const uint64_t q = dq + qs * TILE16, qt = dqt + qs * TILE16;
         const uint64_t kk = dk + ks_ * TILE16, kt = dkt + ks_ * TILE16;
+        const uint64_t oh = doh + ks_ * (OH_BYTES >> 4);
         const uint32_t d = tmem + TM_S + w * 128;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) umma_ss(d, q + 2 * ks, kk + 2 * ks, id_s, ks > 0);
         if constexpr (kTail) umma_ss(d, qt, kt, id_s, 1);
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)  // slab e_ky (k-steps 0-3), slab e_kx (4-7)
+          umma_ts(d, tmem + TM_BQ + 8 * ks, oh + (ks >> 2) * (BQ * 128 >> 4) + 2 * (ks & 3), id_b, 1);
         umma_commit_elect(&s_full[w]);
         umma_commit_elect(&k_empty[ks_]);
-        if (last) umma_commit_elect(&q_empty[qs]);
+        if (last) {
+          umma_commit_elect(&q_empty[qs]);
+          umma_commit_elect(bq_free);
+        }
       };
       auto issue_pv = [&](int c, int w, bool first) {
         const int vs = c % VST;
@@ -244,7 +266,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         tc_fence_after();
         const uint64_t v = dv + vs * TILE16, vt = dvt + vs * TILE16;
         const uint32_t a0 = tmem + TM_S + w * 128;
-        const uint32_t d = tmem + TM_O + w * 128;
+        const uint32_t d = tmem + TM_O + w * 80;
 #pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks) {
           const uint32_t acc = (!first || ks > 0) ? 1u : 0u;
@@ -254,9 +276,9 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         umma_commit_elect(&o_full[w]);
         umma_commit_elect(&v_empty[vs]);
       };
-      // PV(c-1) is issued right after S(c): S(c) goes to the other WG's S buffer, and S(c)
-      // into S_w always follows PV(c-2) (same WG) in issue order, so P_w is read before it
-      // is overwritten (tcgen05.mma executes in order)
+      // PV(c-1) is issued right after S'(c): S'(c) goes to the other WG's S buffer, and S'(c)
+      // into S_w always follows PV(c-2) (same WG) in issue order, so P_w is read before it is
+      // overwritten (tcgen05.mma executes in order)
       int npv[2] = {0, 0};
       int pend_c = -1, pend_w = 0, pend_k = 0;
       bool pend_first = false;
@@ -264,6 +286,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         mbar_wait(&p_full[pend_w], npv[pend_w] & 1);
         if (pend_first && pend_k > 0) mbar_wait(o_free, (pend_k - 1) & 1);  // previous epilogue read O
         tc_fence_after();
+        if (lane == 0 && pend_c == first_c) ZG_TR(pend_k, 15);
         issue_pv(pend_c, pend_w, pend_first);
         npv[pend_w]++;
       };
@@ -271,10 +294,12 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
         const int i = it % nmb;
         const int nc = n_chunks(P, i);
-        mbar_wait(&q_full[k & 1], (k >> 1) & 1);
+        first_c = c;
+        mbar_wait(&q_full[k % QST], (k / QST) & 1);
+        mbar_wait(bq_full, k & 1);
         if (lane == 0) ZG_TR(k, 6);
         for (int j = 0; j < nc; ++j, ++c) {
-          const int w = c & 1;  // chunks alternate WGs across item boundaries too
+          const int w = c & 1;
           issue_s(c, k, w, j == nc - 1);
           if (lane == 0 && j < 6) ZG_TR(k, 7 + j);
           if (pend_c >= 0) flush_pv();
@@ -283,162 +308,150 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
           pend_k = k;
           pend_first = j < 2;  // first chunk of WG w in this item: O_w starts fresh
         }
+        // the item's last PV now: its epilogue (and with it the next item's Bq install, which
+        // the next S' waits for) depends on it
+        flush_pv();
+        pend_c = -1;
       }
-      if (pend_c >= 0) flush_pv();
-    } else if (warp == 2) {
-      // ---------------------------------------------------------- key metadata per chunk
+    } else {
+      // ---------------------------------------------------------- one-hot key rows (warps 2, 3)
+      // chunk c, keys [64*(warp-2), +64): row kr of each SW128 slab = fp16 e_{σk/w} (slab 0) and
+      // e_{σk%w} (slab 1); 16-byte chunk cc of row kr lives at kr*128 + ((cc ^ (kr & 7)) << 4)
+      const uint32_t one = 0x3C00u;  // fp16 1.0
+      const int kbase = (warp - 2) * 64;
       int c = 0;
       for (int it = blockIdx.x; it < P.items; it += gridDim.x) {
         const int i = it % nmb, u = it / nmb / P.heads;
         const int nc = n_chunks(P, i);
         for (int j = 0; j < nc; ++j, ++c) {
-          const int cj = chunk_of(P, i, j), s = c % MST;
-          int ksp[4];
+          const int cj = chunk_of(P, i, j), s = c % KST;
+          int ky[2], kx[2];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int kg = cj * BQ + lane + 32 * q;
-            ksp[q] = kg < P.S ? __ldg(P.k_sp + (long long)u * P.S + kg) : -1;
+          for (int e = 0; e < 2; ++e) {
+            const int kg = cj * BQ + kbase + lane + 32 * e;
+            const int sp = kg < P.S ? __ldg(P.k_sp + (long long)u * P.S + kg) : -1;
+            ky[e] = sp >= 0 ? sp / P.bias_w : -100;
+            kx[e] = sp >= 0 ? sp % P.bias_w : -100;
           }
-          mbar_wait_sleep(&m_empty[s], ((c / MST) & 1) ^ 1);
+          mbar_wait_sleep(&k_empty[s], ((c / KST) & 1) ^ 1);
+          uint8_t* oh = smem + P.off_oh + s * OH_BYTES;
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            koff[s * BQ + lane + 32 * q] =
-                ksp[q] >= 0 ? make_int2((ksp[q] / P.bias_w) * 2, (64 + ksp[q] % P.bias_w) * 2) : make_int2(0, 128);
+          for (int e = 0; e < 2; ++e) {
+            const int kr = kbase + lane + 32 * e;
+            // the two non-zero 16-byte chunks of the row: e_ky in slab 0, e_kx in slab 1
+            const int cy = ky[e] >> 3, cx = 8 + (kx[e] >> 3);
+            uint4 hy = make_uint4(0u, 0u, 0u, 0u), hx = hy;
+            {
+              const uint32_t vy = one << (16 * (ky[e] & 1)), vx = one << (16 * (kx[e] & 1));
+              const int wy = (ky[e] >> 1) & 3, wx = (kx[e] >> 1) & 3;
+              hy.x = wy == 0 ? vy : 0u;
+              hy.y = wy == 1 ? vy : 0u;
+              hy.z = wy == 2 ? vy : 0u;
+              hy.w = wy == 3 ? vy : 0u;
+              hx.x = wx == 0 ? vx : 0u;
+              hx.y = wx == 1 ? vx : 0u;
+              hx.z = wx == 2 ? vx : 0u;
+              hx.w = wx == 3 ? vx : 0u;
+            }
+            const bool live = ky[e] >= 0;
+#pragma unroll
+            for (int cc = 0; cc < 16; ++cc) {
+              const int slab = cc >> 3, c8 = cc & 7;
+              uint4 val = make_uint4(0u, 0u, 0u, 0u);
+              if (live && cc == cy) val = hy;
+              if (live && cc == cx) val = hx;
+              *reinterpret_cast<uint4*>(oh + slab * (BQ * 128) + kr * 128 + ((c8 ^ (kr & 7)) << 4)) = val;
+            }
+          }
+          fence_proxy_async_smem();  // generic-proxy smem writes -> tensor core
           __syncwarp();
-          if (lane == 0) mbar_arrive(&m_full[s]);
-        }
-      }
-    } else {
-      // ---------------------------------------------------------- bias rows of each item (warp 3)
-      // fp16 rows btab[h, σq(r)] (256 B) -> smem rows of 260 B; 16-byte loads (2 rows per
-      // instruction, 32 rows in flight), 4-byte stores.  Double-buffered by item parity.
-      int k = 0;
-      for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
-        const int i = it % nmb, uh = it / nmb, h = uh % P.heads, u = uh / P.heads;
-        const int bb = k & 1;
-        int qsp[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int r = i * BQ + lane + 32 * q;
-          qsp[q] = r < P.S ? __ldg(P.q_sp + (long long)u * P.S + r) : -1;
-        }
-        const __half* tab = P.btab + (long long)h * P.S * 128;
-        uint8_t* dst0 = bias_s + bb * (BQ * 260);
-        const int half = lane >> 4, ch = lane & 15;
-        mbar_wait_sleep(&b_empty[bb], ((k >> 1) & 1) ^ 1);
-        if (lane == 0) ZG_TR(k, 0);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 v[16];
-#pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            const int sp = __shfl_sync(0xffffffffu, qsp[q], 2 * t + half);
-            v[t] = sp >= 0 ? __ldg(reinterpret_cast<const uint4*>(tab + (long long)sp * 128) + ch)
-                           : make_uint4(0u, 0u, 0u, 0u);
-          }
-#pragma unroll
-          for (int t = 0; t < 16; ++t) {
-            uint32_t* d = reinterpret_cast<uint32_t*>(dst0 + (32 * q + 2 * t + half) * 260 + ch * 16);
-            d[0] = v[t].x;
-            d[1] = v[t].y;
-            d[2] = v[t].z;
-            d[3] = v[t].w;
-          }
-        }
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&b_full[bb]);
-          ZG_TR(k, 1);
+          if (lane == 0) mbar_arrive(&oh_full[s]);
         }
       }
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
     // ------------------------------------------------------------ softmax warpgroups
-    const int w = (warp - 4) >> 2;  // WG: chunks j with j % 2 == w
+    const int w = (warp - 4) >> 2;  // WG: chunk ordinals with c % 2 == w
     const int wq = warp & 3;
     const int r = wq * 32 + lane;   // row within the tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
     const uint32_t s_addr = tmem + TM_S + w * 128 + lane_off;
-    const uint32_t o_addr = tmem + TM_O + w * 128 + lane_off;
-    const uint32_t o_oth = tmem + TM_O + (w ^ 1) * 128 + lane_off;
-    const uint8_t* brow0 = bias_s + r * 260;
+    const uint32_t o_addr = tmem + TM_O + w * 80 + lane_off;
+    const uint32_t o_oth = tmem + TM_O + (w ^ 1) * 80 + lane_off;
+    const uint32_t bq_addr = tmem + TM_BQ + w * 32 + lane_off;  // this WG's 64 fp16 bias columns
+    uint8_t* bq_row = smem + P.off_bq + r * BQ_STRIDE + w * 128;
     float* ml = reinterpret_cast<float*>(smem + P.off_ml);  // [item parity][2 wg][2][BQ]: m, l
     constexpr float L2E = 1.4426950408889634f;
     constexpr float kThr = 5.545177444479562f;  // ln 256
-    const float tau = P.tau;
+    const float tau = P.tau, cexp = P.tau * L2E;
+
+    // Bq rows of item `it2` (this WG's half: 64 fp16 = 128 bytes) -> staging smem row (cp.async)
+    auto prefetch_bq = [&](int it2) {
+      if (it2 >= P.items) return;
+      const int i2 = it2 % nmb, uh2 = it2 / nmb, h2 = uh2 % P.heads, u2 = uh2 / P.heads;
+      const int row2 = i2 * BQ + r;
+      if (row2 >= P.S) return;
+      const int sp = __ldg(P.q_sp + (long long)u2 * P.S + row2);
+      const __half* src = P.btab + ((long long)h2 * P.S + sp) * 128 + w * 64;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) cp_async16(bq_row + 16 * q, src + 8 * q);
+    };
+    // staged row -> TMEM (after the previous item's last S' completed)
+    auto install_bq = [&](int k2) {
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      uint32_t v[32];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 x = *reinterpret_cast<const uint4*>(bq_row + 16 * q);
+        v[4 * q] = x.x;
+        v[4 * q + 1] = x.y;
+        v[4 * q + 2] = x.z;
+        v[4 * q + 3] = x.w;
+      }
+      if (k2 > 0) mbar_wait(bq_free, (k2 - 1) & 1);
+      tc_fence_after();
+      tmem_st32(bq_addr, v);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bq_full);
+    };
+
+    prefetch_bq(blockIdx.x);
+    install_bq(0);
     int k = 0, c = 0, nsw = 0;  // nsw: chunks this WG processed (phase of s_full / o_full)
-    (void)c;
     for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
       const int i = it % nmb, uh = it / nmb, h = uh % P.heads, u = uh / P.heads;
       const int nc = n_chunks(P, i);
       const int row = i * BQ + r;
-      mbar_wait(&b_full[k & 1], (k >> 1) & 1);
-      const char* bh_row = reinterpret_cast<const char*>(brow0 + (k & 1) * (BQ * 260));
+      prefetch_bq(it + gridDim.x);  // staging buffer is free: its rows went to TMEM
       if (lane == 0 && wq == 0) ZG_TR(k, 2 + w);
       float m_ref = -INFINITY, ell = 0.f;
       int mine = 0;  // chunks of this item processed by this WG
       for (int j = 0; j < nc; ++j, ++c) {
         if ((c & 1) != w) continue;
-        const int s = c % MST;
-        mbar_wait(&m_full[s], (c / MST) & 1);
-        const int2* ko = koff + s * BQ;
         const int cj = chunk_of(P, i, j);
         const int kvalid = P.S - cj * BQ;  // keys of this chunk below S
-        // bias of a 32-key group (independent of S: overlaps the S MMA / TMEM load latency)
-        auto group_bias = [&](int g, float (&b)[32]) {
-#pragma unroll
-          for (int jj = 0; jj < 32; jj += 2) {
-            const int4 oo = *reinterpret_cast<const int4*>(ko + 32 * g + jj);
-            b[jj] = __half2float(*reinterpret_cast<const __half*>(bh_row + oo.x)) +
-                    __half2float(*reinterpret_cast<const __half*>(bh_row + oo.y));
-            b[jj + 1] = __half2float(*reinterpret_cast<const __half*>(bh_row + oo.z)) +
-                        __half2float(*reinterpret_cast<const __half*>(bh_row + oo.w));
-          }
-        };
-        float bg[32];
-        group_bias(0, bg);
         mbar_wait(&s_full[w], nsw & 1);
         tc_fence_after();
+        if (lane == 0 && wq == 0 && mine == 0 && w == 0) ZG_TR(k, 0);
         uint32_t sr[128];
-        tmem_ld32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(sr));
-        float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          tmem_ld_wait();
-#pragma unroll
-          for (int jj = 0; jj < 32; jj += 2) {
-            const float x0 = fmaf(tau, __uint_as_float(sr[32 * g + jj]), bg[jj]);
-            const float x1 = fmaf(tau, __uint_as_float(sr[32 * g + jj + 1]), bg[jj + 1]);
-            sr[32 * g + jj] = __float_as_uint(x0);
-            sr[32 * g + jj + 1] = __float_as_uint(x1);
-            m0 = fmaxf(m0, x0);
-            m1 = fmaxf(m1, x1);
-          }
-          if (g < 3) {
-            tmem_ld32(s_addr + 32 * (g + 1), *reinterpret_cast<uint32_t(*)[32]>(sr + 32 * (g + 1)));
-            group_bias(g + 1, bg);
-          }
-        }
+        for (int g = 0; g < 4; ++g) tmem_ld32(s_addr + 32 * g, *reinterpret_cast<uint32_t(*)[32]>(sr + 32 * g));
+        tmem_ld_wait();
         if (kvalid < BQ) {
 #pragma unroll
           for (int jj = 0; jj < 128; ++jj)
             if (jj >= kvalid) sr[jj] = __float_as_uint(-INFINITY);
-          m0 = -INFINITY;
-          m1 = -INFINITY;
+        }
+        float m0 = __uint_as_float(sr[0]), m1 = __uint_as_float(sr[1]);
 #pragma unroll
-          for (int jj = 0; jj < 128; jj += 2) {
-            m0 = fmaxf(m0, __uint_as_float(sr[jj]));
-            m1 = fmaxf(m1, __uint_as_float(sr[jj + 1]));
-          }
+        for (int jj = 2; jj < 128; jj += 2) {
+          m0 = fmaxf(m0, __uint_as_float(sr[jj]));
+          m1 = fmaxf(m1, __uint_as_float(sr[jj + 1]));
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&m_empty[s]);
-        if (j >= nc - 2) {  // this WG's last chunk of the item: bias rows no longer needed
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&b_empty[k & 1]);
-        }
-        const float mx = fmaxf(m0, m1);
+        const float mx = tau * fmaxf(m0, m1);  // max logit (tau > 0)
         // lazy rescale: the reference max moves only past the threshold
         float alpha = 1.f;
         if (mx > m_ref + kThr || (m_ref == -INFINITY && mx > -INFINITY)) {
@@ -476,8 +489,9 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
           uint32_t pk[16];
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            const float a = ex2(fmaf(__uint_as_float(sr[32 * g + 2 * q]), L2E, -mc));
-            const float b = ex2(fmaf(__uint_as_float(sr[32 * g + 2 * q + 1]), L2E, -mc));
+            float a, b;
+            ex2x2(fmaf(__uint_as_float(sr[32 * g + 2 * q]), cexp, -mc),
+                  fmaf(__uint_as_float(sr[32 * g + 2 * q + 1]), cexp, -mc), a, b);
             r0 += a;
             r1 += b;
             pk[q] = pack_bf16(a, b);
@@ -489,22 +503,17 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[w]);
+        if (lane == 0 && wq == 0 && mine == 0 && w == 0) ZG_TR(k, 1);
         ++nsw;
         ++mine;
-      }
-      if (mine == 0) {  // no chunk of this item for this WG (nc == 1)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&b_empty[k & 1]);
       }
       // ---- item epilogue: merge the two WGs' partial softmaxes, each WG writes half the columns
       float* mlk = ml + (k & 1) * 4 * BQ;
       mlk[(w * 2 + 0) * BQ + r] = m_ref;
       mlk[(w * 2 + 1) * BQ + r] = ell;
-      // wait for this WG's last PV and the other WG's (its m / l are posted before the barrier)
-      if (mine > 0) mbar_wait(&o_full[w], (nsw - 1) & 1);
-      named_bar_sync(1, 256);
+      if (mine > 0) mbar_wait(&o_full[w], (nsw - 1) & 1);  // this WG's last PV
+      named_bar_sync(1, 256);  // both WGs: m / l posted, both last PVs complete
       const float mo = mlk[((w ^ 1) * 2 + 0) * BQ + r], lo = mlk[((w ^ 1) * 2 + 1) * BQ + r];
-      // the other WG's last PV: it waited for it before the barrier
       const float mm = fmaxf(m_ref, mo);
       const float a_me = (m_ref == -INFINITY) ? 0.f : ex2((m_ref - mm) * L2E);
       const float a_ot = (mo == -INFINITY) ? 0.f : ex2((mo - mm) * L2E);
@@ -555,6 +564,8 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(o_free);
       if (lane == 0 && wq == 0) ZG_TR(k, 4 + w);
+      // next item's bias rows into TMEM once this item's last S' has completed
+      if (it + (int)gridDim.x < P.items) install_bq(k + 1);
     }
   }
   tc_fence_before();
@@ -567,20 +578,19 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
 
 using namespace zs;
 
-// Host launcher: returns 1 when outside this kernel's envelope (b_row = b_col = 128, square
-// grids, dh 64 / 80), 0 on launch, negative on error.
+// Host launcher: returns 1 when outside this kernel's envelope (b_row = b_col = 128, bias
+// width <= 64, dh 64 / 80), 0 on launch, negative on error.
 int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                      long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
                      const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
                      float tau, void* out, long long ldo, long long ous, cudaStream_t st) {
   using namespace attng;
-  if (b_row != BQ || b_col != BQ || (dh != 64 && dh != 80) || S < 1 || bias_w > 64) return 1;
+  if (b_row != BQ || b_col != BQ || (dh != 64 && dh != 80) || S < 1 || bias_w > 64 || !(tau > 0.f)) return 1;
   Params p{};
   p.units = units;
   p.heads = heads;
   p.S = S;
   p.bias_w = bias_w;
-  p.W1 = 130;
   p.T = (S + BQ - 1) / BQ;
   p.prefix = prefix;
   const long long items = (long long)units * heads * p.T;
@@ -602,16 +612,16 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
     off += bytes;
     return o;
   };
-  p.off_q = take(2 * tile, 1024);
+  p.off_q = take(QST * tile, 1024);
   p.off_k = take(KST * tile, 1024);
+  p.off_oh = take(KST * OH_BYTES, 1024);
   p.off_v = take(VST * tile, 1024);
-  p.off_bias = take(2 * BQ * 260, 16);
-  p.off_koff = take(MST * BQ * 8, 16);
+  p.off_bq = take(BQ * BQ_STRIDE, 16);
   p.off_ml = take(2 * 4 * BQ * 4, 16);
-  p.off_bar = take(512, 8);
+  p.off_bar = take(256, 8);
   const size_t smem = 1024 + (size_t)off;
   if (smem > 227 * 1024) return 1;
-  // fp16 bias rows [heads, S, 128] (scratch, grow-only per device)
+  // fp16 bias operand rows [heads, S, 128] (scratch, grow-only per device)
   {
     static __half* buf[64] = {nullptr};
     static size_t cap[64] = {0};
@@ -626,7 +636,8 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
       cap[dev] = need;
     }
     const long long n = (long long)need;
-    glob_bias_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(bh, bw, heads * S, bias_w, buf[dev]);
+    glob_bias_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(bh, bw, heads * S, bias_w, 1.0f / tau,
+                                                                        buf[dev]);
     p.btab = buf[dev];
   }
   CUtensorMap m[6];

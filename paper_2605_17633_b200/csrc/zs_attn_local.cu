@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(attnl::kThreads, 1)
   uint64_t* ki_empty = bar + 20; // [item parity] (256 arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 24);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index via shfl: provably warp-uniform, so role code can use uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int nck = (P.sk + BKC - 1) / BKC;     // 1 or 2 key chunks
   const bool has_b = P.sq > BQ;
   const unsigned mask_a = P.mask[0], mask_b = has_b ? P.mask[1] : 0u;

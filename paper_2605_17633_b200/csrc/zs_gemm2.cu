@@ -128,7 +128,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
   float* xstage = reinterpret_cast<float*>(smem + kStages * STAGE_BYTES + 256);  // [8 warps][32][XS]
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index via shfl: provably warp-uniform, so role code can use uniform registers
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
 
