@@ -178,7 +178,9 @@ ZS_API int zs_rc_mlp_fwd(float* x, long long ldx, const int32_t* keep_rows, int 
  * im2col for non-overlapping PxP patches of an fp32 NCHW image batch:
  *   out [B*(H/P)*(W/P), 3*P*P] bf16, column order (c, ky, kx) = Conv2d weight flattening. */
 ZS_API int zs_patchify(const float* img, int B, int Cin, int H, int W, int P, void* out, zs_stream_t stream);
-/* 3x3 / pad 1 im2col of a channels-last bf16 map [B, H, W, C] -> [B*H*W, 9*C], column order (c, ky, kx). */
+/* 3x3 / pad 1 im2col of a channels-last bf16 map [B, H, W, C] -> [B*H*W, 9*C], tap-major column
+ * order (ky, kx, c) (contiguous channel runs); the matching weight is Conv2d's [O, C, 3, 3]
+ * permuted to [O, 3, 3, C].  C % 8 == 0, 16-byte aligned pointers. */
 ZS_API int zs_im2col3x3(const void* x, int B, int H, int W, int C, void* out, zs_stream_t stream);
 
 #ifdef __cplusplus

@@ -96,7 +96,7 @@ int launch_layernorm(const float* x, long long ldx, const int* rows, const int* 
   if (n <= 0) return 0;
   if (!x || !g || !b || !out) return ZS_ERR_ARG;
   if (C <= 0 || C % 4 || C > 2048 || ldx % 4 || (out_f32 ? ldo % 4 : ldo % 4)) return ZS_ERR_SHAPE;
-  const int grid = grid_for_rows(n, 8);
+  const int grid = grid_for_rows(n, 8);  // one warp per row, 8 rows per CTA
   if (out_f32)
     ln_rows_kernel<true><<<grid, 256, 0, st>>>(x, ldx, rows, out_rows, n, n_dev, C, g, b, eps, out, ldo);
   else
@@ -281,21 +281,25 @@ __global__ void patchify_kernel(const float* __restrict__ img, int B, int Cin, i
     out[e] = __float2bfloat16_rn(img[(((long long)b * Cin + c) * H + y) * W + x]);
   }
 }
+// 3x3 / stride 1 / pad 1 im2col of channels-last bf16 rows, TAP-MAJOR columns:
+// out[row, (ky*3 + kx)*C + c] = x[b, y+ky-1, x+kx-1, c] (zeros outside).  One thread moves 8
+// channels (16 bytes): reads and writes are contiguous runs of C channels.
 __global__ void im2col3x3_kernel(const __nv_bfloat16* __restrict__ x, int B, int H, int W, int C,
                                  __nv_bfloat16* __restrict__ out) {
-  const long long ncol = 9LL * C;
-  const long long total = (long long)B * H * W * ncol;
+  const int cv = C >> 3;  // 16-byte vectors per pixel
+  const long long total = (long long)B * H * W * 9 * cv;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
-    const long long row = e / ncol;
-    const int col = (int)(e % ncol);
-    const int c = col / 9, ky = (col / 3) % 3, kx = col % 3;
-    const int b = (int)(row / (H * W));
-    const int t = (int)(row % (H * W));
-    const int y = t / W + ky - 1, xx = t % W + kx - 1;
-    __nv_bfloat16 v = __float2bfloat16_rn(0.f);
-    if (y >= 0 && y < H && xx >= 0 && xx < W) v = x[(((long long)b * H + y) * W + xx) * C + c];
-    out[e] = v;
+    const int v = (int)(e % cv);
+    const long long rt = e / cv;
+    const int tap = (int)(rt % 9);
+    const long long row = rt / 9;
+    const int b = (int)(row / (H * W)), t = (int)(row % (H * W));
+    const int y = t / W + tap / 3 - 1, xx = t % W + tap % 3 - 1;
+    uint4 val = make_uint4(0u, 0u, 0u, 0u);
+    if (y >= 0 && y < H && xx >= 0 && xx < W)
+      val = reinterpret_cast<const uint4*>(x + (((long long)b * H + y) * W + xx) * C)[v];
+    reinterpret_cast<uint4*>(out + row * 9LL * C + (long long)tap * C)[v] = val;
   }
 }
 
@@ -402,6 +406,7 @@ extern "C" int zs_patchify(const float* img, int B, int Cin, int H, int W, int P
 extern "C" int zs_im2col3x3(const void* x, int B, int H, int W, int C, void* out, zs_stream_t stream) {
   if (B <= 0) return 0;
   if (!x || !out) return ZS_ERR_ARG;
+  if (C % 8 || (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out)) & 15) return ZS_ERR_ALIGN;
   im2col3x3_kernel<<<num_sms() * 8, 256, 0, S(stream)>>>(reinterpret_cast<const __nv_bfloat16*>(x), B, H, W, C,
                                                           reinterpret_cast<__nv_bfloat16*>(out));
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;

@@ -274,6 +274,9 @@ class SparseSAMImageEncoder:
         self.core = StripeSortEncoder(cfg, params, device)
         self.device = self.core.device
         self._buf_B = None
+        # 3x3 neck conv weight [256, 256*9] (c, ky, kx) -> tap-major (ky, kx, c) to match im2col3x3
+        self._neck2_tap = (frame.neck2_w.view(SAM_NECK, SAM_NECK, 3, 3).permute(0, 2, 3, 1)
+                           .reshape(SAM_NECK, 9 * SAM_NECK).contiguous())
 
     def _bufs(self, B: int) -> dict:
         if self._buf_B != B:
@@ -299,22 +302,27 @@ class SparseSAMImageEncoder:
         K.gemm(patches, f.pe_w, f.pe_b, epi=K.EPI_F32_RESID, out=bufs["x0"], res=f.pos, res_mod=self.cfg.grid.n())
         return bufs["x0"]
 
-    def neck(self, rows: torch.Tensor, B: int) -> torch.Tensor:
+    def neck(self, rows: torch.Tensor, B: int, out: torch.Tensor | None = None) -> torch.Tensor:
         f = self.frame
         bufs = self._bufs(B)
         g = self.cfg.grid
         xb = K.cast_rows_bf16(rows, out=bufs["xb16"])
         K.gemm(xb, f.neck1_w, None, epi=K.EPI_F32_RESID, out=bufs["n1"])
         K.layernorm_rows(bufs["n1"], f.neck_ln1_g, f.neck_ln1_b, out=bufs["n1b"])
-        cols = K.im2col3x3(bufs["n1b"].view(B, g.h, g.w, SAM_NECK))
-        K.gemm(cols, f.neck2_w, None, epi=K.EPI_F32_RESID, out=bufs["n2"])
-        K.layernorm_rows(bufs["n2"], f.neck_ln2_g, f.neck_ln2_b, out_f32=True, out=bufs["out"])
-        return bufs["out"].view(B, g.h, g.w, SAM_NECK)
+        cols = K.im2col3x3(bufs["n1b"].view(B, g.h, g.w, SAM_NECK))  # tap-major (ky, kx, c) columns
+        K.gemm(cols, self._neck2_tap, None, epi=K.EPI_F32_RESID, out=bufs["n2"])
+        if out is None:
+            out = bufs["out"]
+        elif tuple(out.shape) not in ((B, g.h, g.w, SAM_NECK), (B * g.h * g.w, SAM_NECK)) or out.dtype != torch.float32:
+            raise ValueError(f"out must be float32 [B, {g.h}, {g.w}, {SAM_NECK}]")
+        K.layernorm_rows(bufs["n2"], f.neck_ln2_g, f.neck_ln2_b, out_f32=True, out=out.view(B * g.h * g.w, SAM_NECK))
+        return out.view(B, g.h, g.w, SAM_NECK)
 
-    def __call__(self, img: torch.Tensor, mode: str = "sparse") -> torch.Tensor:
-        """[B, 3, 1024, 1024] fp32 -> channels-last embeddings [B, 64, 64, 256] fp32."""
+    def __call__(self, img: torch.Tensor, mode: str = "sparse", out: torch.Tensor | None = None) -> torch.Tensor:
+        """[B, 3, 1024, 1024] fp32 -> channels-last embeddings [B, 64, 64, 256] fp32 (into ``out``
+        when given, so a caller can double-buffer results while copying the previous ones out)."""
         B = img.shape[0]
         g = self.cfg.grid
         x0 = self.embed(img)
         xo = self.core.forward_rows(x0.view(B, g.h, g.w, self.cfg.d), mode, out=self._bufs(B)["xo"])
-        return self.neck(xo, B)
+        return self.neck(xo, B, out=out)

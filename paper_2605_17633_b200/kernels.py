@@ -317,6 +317,7 @@ def patchify(img: torch.Tensor, patch: int) -> torch.Tensor:
 
 
 def im2col3x3(x: torch.Tensor) -> torch.Tensor:
+    """[B, H, W, C] bf16 -> [B*H*W, 9*C], tap-major columns (ky, kx, c)."""
     _need(x, torch.bfloat16, "x")
     B, H, W, Cc = x.shape
     out = torch.empty((B * H * W, 9 * Cc), device=x.device, dtype=torch.bfloat16)

@@ -310,3 +310,14 @@ def test_attention_general_tiles_many_items():
             ref = O.masked_attention_f64(qf[rows, :dh], qf[rows, C:C + dh], qf[rows, 2 * C:2 * C + dh],
                                          bh[0].cpu().numpy(), bw[0].cpu().numpy(), s, s, br, bc, r, 0.125)
             assert rel(out[rows, :dh].float(), ref) < 1e-2, (br, bc, r)
+
+
+def test_im2col3x3_tap_major():
+    """Neck 3x3 im2col: tap-major columns (ky, kx, c), zero padding, exact copy."""
+    g = torch.Generator().manual_seed(4)
+    x = torch.randn(2, 5, 7, 16, generator=g).bfloat16().to(DEV)
+    out = K.im2col3x3(x)
+    xp = torch.nn.functional.pad(x.permute(0, 3, 1, 2).float(), (1, 1, 1, 1))
+    ref = torch.stack([xp[:, :, ky:ky + 5, kx:kx + 7] for ky in range(3) for kx in range(3)], dim=-1)
+    ref = ref.permute(0, 2, 3, 4, 1).reshape(2 * 5 * 7, 9 * 16)
+    assert torch.equal(out.float(), ref)
