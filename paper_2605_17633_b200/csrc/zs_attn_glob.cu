@@ -17,8 +17,8 @@
 //    item (each WG writes half of the output columns).
 //  * P (bf16) overwrites the WG's S columns in TMEM and is the A operand of the PV MMA.
 //  * Lazy rescaling: O_w is rescaled in TMEM only when the row max grows by more than ln 256.
-//  * The next item's Bq rows are prefetched with cp.async while the current item runs and
-//    written into TMEM (tcgen05.st) once its last S' MMA has completed.
+//  * The next item's Bq rows are loaded from the fp16 table and written into TMEM
+//    (tcgen05.st) by the softmax threads once the item's last S' MMA has completed.
 // Roles: warp 0 TMA (lane 0: Q per item + K per chunk, lane 1: V per chunk), warp 1 MMA (whole
 // warp, elected lane), warps 2-3 one-hot key rows per chunk, warps 4-7 WG0, warps 8-11 WG1.
 #include <cuda_fp16.h>
@@ -35,14 +35,14 @@ namespace attng {
 constexpr int BQ = 128;
 constexpr int kThreads = 384;
 constexpr uint32_t kTmemCols = 512;
-constexpr int KST = 2;  // K + one-hot ring stages
+constexpr int KST = 3;  // K ring stages
+constexpr int OST = 2;  // one-hot ring stages (generated on chip: no memory latency to hide)
 constexpr int QST = 1;  // Q slots (the next item's Q loads once the last S' of the item completed)
 constexpr int VST = 3;  // V ring stages
 constexpr uint32_t TM_S = 0;     // S_w at [w*128, w*128+128)
 constexpr uint32_t TM_O = 256;   // O_w at 256 + w*80
 constexpr uint32_t TM_BQ = 416;  // Bq: 128 fp16 = 64 columns
 constexpr int OH_BYTES = 2 * BQ * 128;  // two 64-column SW128 slabs (e_ky | e_kx)
-constexpr int BQ_STRIDE = 272;          // bytes per staged Bq row (256 + 16 pad)
 
 struct Params {
   int units, heads, S, bias_w, T, prefix, items;
@@ -52,7 +52,7 @@ struct Params {
   const int* k_sp;
   float tau;
   __nv_bfloat16* out;
-  int off_q, off_k, off_oh, off_v, off_bq, off_ml, off_bar, tile;
+  int off_q, off_k, off_oh, off_v, off_ml, off_bar, tile;
   int trace;
 };
 
@@ -114,12 +114,28 @@ __global__ void glob_bias_prep_kernel(const float* __restrict__ bh, const float*
 
 }  // namespace attng
 
-// Debug timeline (ZS_GLOB_TRACE=1): clock64() stamps of CTA 0's first items, 16 slots per item.
+// Debug timeline: build with -DZS_KERNEL_TRACE and run with ZS_GLOB_TRACE=1 to record clock64()
+// stamps of CTA 0 (16 slots per item; 8 per chunk of item 5).  Compiled out by default: the
+// stamps sit on the MMA issue path and would cost its uniform-datapath code.
 __device__ unsigned long long g_glob_trace[64 * 16];
+__device__ unsigned long long g_glob_trace2[128];
+#ifdef ZS_KERNEL_TRACE
 #define ZG_TR(k, slot)                                                                       \
   do {                                                                                       \
     if (P.trace && blockIdx.x == 0 && (k) < 64) g_glob_trace[(k) * 16 + (slot)] = clock64(); \
   } while (0)
+#define ZG_T2(k, j, slot)                                                                                  \
+  do {                                                                                                     \
+    if (P.trace && blockIdx.x == 0 && (k) == 5 && (j) < 16) g_glob_trace2[(j) * 8 + (slot)] = clock64(); \
+  } while (0)
+#else
+#define ZG_TR(k, slot) \
+  do {             \
+  } while (0)
+#define ZG_T2(k, j, slot) \
+  do {                \
+  } while (0)
+#endif
 
 template <int DH>
 __global__ void __launch_bounds__(attng::kThreads, 1)
@@ -136,8 +152,8 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
   uint64_t* q_full = bar + 0;    // [QST]
   uint64_t* q_empty = bar + 2;   // [QST]
   uint64_t* k_full = bar + 4;    // [KST] K tile landed (TMA)
-  uint64_t* k_empty = bar + 8;   // [KST] S' of the chunk done: K and one-hot stage free
-  uint64_t* oh_full = bar + 12;  // [KST] one-hot rows written (warps 2, 3)
+  uint64_t* k_empty = bar + 8;   // [KST] S' of the chunk done: K stage free
+  uint64_t* oh_full = bar + 12;  // [OST] one-hot rows written (warps 2, 3)
   uint64_t* v_full = bar + 16;   // [VST]
   uint64_t* v_empty = bar + 20;  // [VST]
   uint64_t* s_full = bar + 24;   // [wg]
@@ -146,8 +162,9 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
   uint64_t* o_free = bar + 30;   // 8 warps: O_0 / O_1 read by the item's epilogue
   uint64_t* bq_full = bar + 31;  // 8 warps: the item's Bq rows are in TMEM
   uint64_t* bq_free = bar + 32;  // the item's last S' completed (Bq may be replaced)
+  uint64_t* oh_empty = bar + 36; // [OST] S' of the chunk done: one-hot stage free
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 34);
-  static_assert(KST <= 4 && VST <= 4 && QST <= 2, "barrier slots");
+  static_assert(KST <= 4 && VST <= 4 && QST <= 2 && OST <= 4, "barrier slots");
 
   // warp index via shfl: provably warp-uniform, so role code can use uniform registers
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -168,7 +185,10 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     for (int s = 0; s < KST; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < OST; ++s) {
       mbar_init(&oh_full[s], 2);
+      mbar_init(&oh_empty[s], 1);
     }
     for (int s = 0; s < VST; ++s) {
       mbar_init(&v_full[s], 1);
@@ -237,15 +257,17 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       // S'(c) of chunk ordinal c into S_w: q.k (bf16) then + Bq . OH^T (fp16, A from TMEM)
       int first_c = 0;  // chunk ordinal of the current item's first chunk (trace only)
       auto issue_s = [&](int c, int k, int w, bool last) {
-        const int ks_ = c % KST, qs = k % QST;
+        const int ks_ = c % KST, os_ = c % OST, qs = k % QST;
         mbar_wait(&k_full[ks_], (c / KST) & 1);
         if (lane == 0 && c == first_c + 1) ZG_TR(k, 13);
-        mbar_wait(&oh_full[ks_], (c / KST) & 1);
+        if (lane == 0) ZG_T2(k, c - first_c, 4);
+        mbar_wait(&oh_full[os_], (c / OST) & 1);
         if (lane == 0 && c == first_c + 1) ZG_TR(k, 14);
+        if (lane == 0) ZG_T2(k, c - first_c, 5);
         tc_fence_after();
         const uint64_t q = dq + qs * TILE16, qt = dqt + qs * TILE16;
         const uint64_t kk = dk + ks_ * TILE16, kt = dkt + ks_ * TILE16;
-        const uint64_t oh = doh + ks_ * (OH_BYTES >> 4);
+        const uint64_t oh = doh + os_ * (OH_BYTES >> 4);
         const uint32_t d = tmem + TM_S + w * 128;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) umma_ss(d, q + 2 * ks, kk + 2 * ks, id_s, ks > 0);
@@ -255,6 +277,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
           umma_ts(d, tmem + TM_BQ + 8 * ks, oh + (ks >> 2) * (BQ * 128 >> 4) + 2 * (ks & 3), id_b, 1);
         umma_commit_elect(&s_full[w]);
         umma_commit_elect(&k_empty[ks_]);
+        umma_commit_elect(&oh_empty[os_]);
         if (last) {
           umma_commit_elect(&q_empty[qs]);
           umma_commit_elect(bq_free);
@@ -288,6 +311,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         tc_fence_after();
         if (lane == 0 && pend_c == first_c) ZG_TR(pend_k, 15);
         issue_pv(pend_c, pend_w, pend_first);
+        if (lane == 0) ZG_T2(pend_k, pend_c - first_c, 3);
         npv[pend_w]++;
       };
       int k = 0, c = 0;
@@ -302,6 +326,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
           const int w = c & 1;
           issue_s(c, k, w, j == nc - 1);
           if (lane == 0 && j < 6) ZG_TR(k, 7 + j);
+          if (lane == 0) ZG_T2(k, j, 0);
           if (pend_c >= 0) flush_pv();
           pend_c = c;
           pend_w = w;
@@ -316,57 +341,87 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     } else {
       // ---------------------------------------------------------- one-hot key rows (warps 2, 3)
       // chunk c, keys [64*(warp-2), +64): row kr of each SW128 slab = fp16 e_{σk/w} (slab 0) and
-      // e_{σk%w} (slab 1); 16-byte chunk cc of row kr lives at kr*128 + ((cc ^ (kr & 7)) << 4)
+      // e_{σk%w} (slab 1); 16-byte chunk cc of row kr lives at kr*128 + ((cc ^ (kr & 7)) << 4).
+      // The stage buffers are zeroed once; per chunk a lane clears the two hot chunks its row
+      // had in that stage and writes the two new ones (4 stores instead of 16).  The next
+      // chunk's key indices are loaded while the current chunk is written.
       const uint32_t one = 0x3C00u;  // fp16 1.0
       const int kbase = (warp - 2) * 64;
-      int c = 0;
-      for (int it = blockIdx.x; it < P.items; it += gridDim.x) {
-        const int i = it % nmb, u = it / nmb / P.heads;
-        const int nc = n_chunks(P, i);
-        for (int j = 0; j < nc; ++j, ++c) {
-          const int cj = chunk_of(P, i, j), s = c % KST;
-          int ky[2], kx[2];
+      const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int kg = cj * BQ + kbase + lane + 32 * e;
-            const int sp = kg < P.S ? __ldg(P.k_sp + (long long)u * P.S + kg) : -1;
-            ky[e] = sp >= 0 ? sp / P.bias_w : -100;
-            kx[e] = sp >= 0 ? sp % P.bias_w : -100;
-          }
-          mbar_wait_sleep(&k_empty[s], ((c / KST) & 1) ^ 1);
-          uint8_t* oh = smem + P.off_oh + s * OH_BYTES;
+      for (int st = 0; st < OST; ++st)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int kr = kbase + lane + 32 * e;
+#pragma unroll
+          for (int cc = 0; cc < 16; ++cc)
+            *reinterpret_cast<uint4*>(smem + P.off_oh + st * OH_BYTES + (cc >> 3) * (BQ * 128) + kr * 128 +
+                                      (((cc & 7) ^ (kr & 7)) << 4)) = z4;
+        }
+      int prev[OST][2][2];  // byte offsets of the hot chunks last written per stage / row (-1: none)
+#pragma unroll
+      for (int st = 0; st < OST; ++st)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) prev[st][e][0] = prev[st][e][1] = -1;
+      auto load_sp = [&](int it_, int j_, int (&sp)[2]) {
+        const int i_ = it_ % nmb, u_ = it_ / nmb / P.heads, cj = chunk_of(P, i_, j_);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int kg = cj * BQ + kbase + lane + 32 * e;
+          sp[e] = kg < P.S ? __ldg(P.k_sp + (long long)u_ * P.S + kg) : -1;
+        }
+      };
+      int it = blockIdx.x, j = 0, kk2 = 0;
+      int spc[2] = {-1, -1};
+      if (it < P.items) load_sp(it, 0, spc);
+      for (int c = 0; it < P.items; ++c) {
+        const int nc = n_chunks(P, it % nmb);
+        int it2 = it, j2 = j + 1;
+        if (j2 == nc) {
+          it2 += gridDim.x;
+          j2 = 0;
+        }
+        int spn[2] = {-1, -1};
+        if (it2 < P.items) load_sp(it2, j2, spn);  // in flight while this chunk is written
+        const int st = c % OST;
+        mbar_wait_sleep(&oh_empty[st], ((c / OST) & 1) ^ 1);
+        if (lane == 0 && warp == 2) ZG_T2(kk2, j, 7);
+        uint8_t* oh = smem + P.off_oh + st * OH_BYTES;
+        // stage index made compile-time (unrolled + matched) so prev[][][] stays in registers
+#pragma unroll
+        for (int sidx = 0; sidx < OST; ++sidx) {
+          if (sidx != st) continue;
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int kr = kbase + lane + 32 * e;
-            // the two non-zero 16-byte chunks of the row: e_ky in slab 0, e_kx in slab 1
-            const int cy = ky[e] >> 3, cx = 8 + (kx[e] >> 3);
-            uint4 hy = make_uint4(0u, 0u, 0u, 0u), hx = hy;
-            {
-              const uint32_t vy = one << (16 * (ky[e] & 1)), vx = one << (16 * (kx[e] & 1));
-              const int wy = (ky[e] >> 1) & 3, wx = (kx[e] >> 1) & 3;
-              hy.x = wy == 0 ? vy : 0u;
-              hy.y = wy == 1 ? vy : 0u;
-              hy.z = wy == 2 ? vy : 0u;
-              hy.w = wy == 3 ? vy : 0u;
-              hx.x = wx == 0 ? vx : 0u;
-              hx.y = wx == 1 ? vx : 0u;
-              hx.z = wx == 2 ? vx : 0u;
-              hx.w = wx == 3 ? vx : 0u;
-            }
-            const bool live = ky[e] >= 0;
-#pragma unroll
-            for (int cc = 0; cc < 16; ++cc) {
-              const int slab = cc >> 3, c8 = cc & 7;
-              uint4 val = make_uint4(0u, 0u, 0u, 0u);
-              if (live && cc == cy) val = hy;
-              if (live && cc == cx) val = hx;
-              *reinterpret_cast<uint4*>(oh + slab * (BQ * 128) + kr * 128 + ((c8 ^ (kr & 7)) << 4)) = val;
+            if (prev[sidx][e][0] >= 0) *reinterpret_cast<uint4*>(oh + prev[sidx][e][0]) = z4;
+            if (prev[sidx][e][1] >= 0) *reinterpret_cast<uint4*>(oh + prev[sidx][e][1]) = z4;
+            prev[sidx][e][0] = prev[sidx][e][1] = -1;
+            const int sp = spc[e];
+            if (sp >= 0) {
+              const int ky = sp / P.bias_w, kx = sp % P.bias_w;
+              const int oy = kr * 128 + (((ky >> 3) ^ (kr & 7)) << 4);
+              const int ox = BQ * 128 + kr * 128 + (((kx >> 3) ^ (kr & 7)) << 4);
+              const uint32_t vy = one << (16 * (ky & 1)), vx = one << (16 * (kx & 1));
+              const int wy = (ky >> 1) & 3, wx = (kx >> 1) & 3;
+              *reinterpret_cast<uint4*>(oh + oy) =
+                  make_uint4(wy == 0 ? vy : 0u, wy == 1 ? vy : 0u, wy == 2 ? vy : 0u, wy == 3 ? vy : 0u);
+              *reinterpret_cast<uint4*>(oh + ox) =
+                  make_uint4(wx == 0 ? vx : 0u, wx == 1 ? vx : 0u, wx == 2 ? vx : 0u, wx == 3 ? vx : 0u);
+              prev[sidx][e][0] = oy;
+              prev[sidx][e][1] = ox;
             }
           }
-          fence_proxy_async_smem();  // generic-proxy smem writes -> tensor core
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&oh_full[s]);
         }
+        fence_proxy_async_smem();  // generic-proxy smem writes -> tensor core
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&oh_full[st]);
+        if (lane == 0 && warp == 2) ZG_T2(kk2, j, 6);
+        spc[0] = spn[0];
+        spc[1] = spn[1];
+        if (it2 != it) ++kk2;
+        it = it2;
+        j = j2;
       }
     }
   } else {
@@ -380,34 +435,33 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     const uint32_t o_addr = tmem + TM_O + w * 80 + lane_off;
     const uint32_t o_oth = tmem + TM_O + (w ^ 1) * 80 + lane_off;
     const uint32_t bq_addr = tmem + TM_BQ + w * 32 + lane_off;  // this WG's 64 fp16 bias columns
-    uint8_t* bq_row = smem + P.off_bq + r * BQ_STRIDE + w * 128;
     float* ml = reinterpret_cast<float*>(smem + P.off_ml);  // [item parity][2 wg][2][BQ]: m, l
     constexpr float L2E = 1.4426950408889634f;
     constexpr float kThr = 5.545177444479562f;  // ln 256
     const float tau = P.tau, cexp = P.tau * L2E;
 
-    // Bq rows of item `it2` (this WG's half: 64 fp16 = 128 bytes) -> staging smem row (cp.async)
-    auto prefetch_bq = [&](int it2) {
-      if (it2 >= P.items) return;
+    // Bq rows of item `it2` (this WG's half: 64 fp16 = 128 bytes) -> TMEM, once the previous
+    // item's last S' has completed (bq_free)
+    auto install_bq = [&](int it2, int k2) {
+      uint4 x[8];
       const int i2 = it2 % nmb, uh2 = it2 / nmb, h2 = uh2 % P.heads, u2 = uh2 / P.heads;
       const int row2 = i2 * BQ + r;
-      if (row2 >= P.S) return;
-      const int sp = __ldg(P.q_sp + (long long)u2 * P.S + row2);
-      const __half* src = P.btab + ((long long)h2 * P.S + sp) * 128 + w * 64;
+      if (row2 < P.S) {
+        const int sp = __ldg(P.q_sp + (long long)u2 * P.S + row2);
+        const uint4* src = reinterpret_cast<const uint4*>(P.btab + ((long long)h2 * P.S + sp) * 128 + w * 64);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) cp_async16(bq_row + 16 * q, src + 8 * q);
-    };
-    // staged row -> TMEM (after the previous item's last S' completed)
-    auto install_bq = [&](int k2) {
-      asm volatile("cp.async.wait_all;" ::: "memory");
+        for (int q = 0; q < 8; ++q) x[q] = __ldg(src + q);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q] = make_uint4(0u, 0u, 0u, 0u);
+      }
       uint32_t v[32];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const uint4 x = *reinterpret_cast<const uint4*>(bq_row + 16 * q);
-        v[4 * q] = x.x;
-        v[4 * q + 1] = x.y;
-        v[4 * q + 2] = x.z;
-        v[4 * q + 3] = x.w;
+        v[4 * q] = x[q].x;
+        v[4 * q + 1] = x[q].y;
+        v[4 * q + 2] = x[q].z;
+        v[4 * q + 3] = x[q].w;
       }
       if (k2 > 0) mbar_wait(bq_free, (k2 - 1) & 1);
       tc_fence_after();
@@ -418,14 +472,12 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       if (lane == 0) mbar_arrive(bq_full);
     };
 
-    prefetch_bq(blockIdx.x);
-    install_bq(0);
+    install_bq(blockIdx.x, 0);
     int k = 0, c = 0, nsw = 0;  // nsw: chunks this WG processed (phase of s_full / o_full)
     for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
       const int i = it % nmb, uh = it / nmb, h = uh % P.heads, u = uh / P.heads;
       const int nc = n_chunks(P, i);
       const int row = i * BQ + r;
-      prefetch_bq(it + gridDim.x);  // staging buffer is free: its rows went to TMEM
       if (lane == 0 && wq == 0) ZG_TR(k, 2 + w);
       float m_ref = -INFINITY, ell = 0.f;
       int mine = 0;  // chunks of this item processed by this WG
@@ -436,6 +488,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         mbar_wait(&s_full[w], nsw & 1);
         tc_fence_after();
         if (lane == 0 && wq == 0 && mine == 0 && w == 0) ZG_TR(k, 0);
+        if (lane == 0 && wq == 0) ZG_T2(k, j, 1);
         uint32_t sr[128];
 #pragma unroll
         for (int g = 0; g < 4; ++g) tmem_ld32(s_addr + 32 * g, *reinterpret_cast<uint32_t(*)[32]>(sr + 32 * g));
@@ -504,6 +557,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[w]);
         if (lane == 0 && wq == 0 && mine == 0 && w == 0) ZG_TR(k, 1);
+        if (lane == 0 && wq == 0) ZG_T2(k, j, 2);
         ++nsw;
         ++mine;
       }
@@ -565,7 +619,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       if (lane == 0) mbar_arrive(o_free);
       if (lane == 0 && wq == 0) ZG_TR(k, 4 + w);
       // next item's bias rows into TMEM once this item's last S' has completed
-      if (it + (int)gridDim.x < P.items) install_bq(k + 1);
+      if (it + (int)gridDim.x < P.items) install_bq(it + gridDim.x, k + 1);
     }
   }
   tc_fence_before();
@@ -614,9 +668,8 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
   };
   p.off_q = take(QST * tile, 1024);
   p.off_k = take(KST * tile, 1024);
-  p.off_oh = take(KST * OH_BYTES, 1024);
+  p.off_oh = take(OST * OH_BYTES, 1024);
   p.off_v = take(VST * tile, 1024);
-  p.off_bq = take(BQ * BQ_STRIDE, 16);
   p.off_ml = take(2 * 4 * BQ * 4, 16);
   p.off_bar = take(256, 8);
   const size_t smem = 1024 + (size_t)off;
@@ -669,6 +722,10 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
 }
 
 extern "C" __attribute__((visibility("default"))) int zs_debug_glob_trace(unsigned long long* host, int n) {
-  if (n > 64 * 16) n = 64 * 16;
-  return cudaMemcpyFromSymbol(host, g_glob_trace, n * sizeof(unsigned long long)) == cudaSuccess ? 0 : -1;
+  if (n > 64 * 16 + 128) n = 64 * 16 + 128;
+  if (cudaMemcpyFromSymbol(host, g_glob_trace, (n < 1024 ? n : 1024) * sizeof(unsigned long long)) != cudaSuccess)
+    return -1;
+  if (n > 1024 && cudaMemcpyFromSymbol(host + 1024, g_glob_trace2, (n - 1024) * sizeof(unsigned long long)) != cudaSuccess)
+    return -1;
+  return 0;
 }

@@ -200,12 +200,19 @@ __global__ void win_bias_prep_kernel(const float* __restrict__ bh, const float* 
 
 }  // namespace attnw
 
-// Debug timeline (ZS_WIN_TRACE=1): clock64() stamps of CTA 0's first items, 32 slots per item.
+// Debug timeline: build with -DZS_KERNEL_TRACE and run with ZS_WIN_TRACE=1 to record clock64()
+// stamps of CTA 0's first items (32 slots per item).  Compiled out by default.
 __device__ unsigned long long g_win_trace[64 * 32];
+#ifdef ZS_KERNEL_TRACE
 #define ZS_TR(k, slot)                                                                      \
   do {                                                                                      \
     if (P.trace && blockIdx.x == 0 && (k) < 64) g_win_trace[(k) * 32 + (slot)] = clock64(); \
   } while (0)
+#else
+#define ZS_TR(k, slot) \
+  do {             \
+  } while (0)
+#endif
 
 // REG: all live groups of a row fit in registers (<= 3 groups of 32); otherwise S' is
 // re-read from TMEM for the exp pass.

@@ -26,11 +26,18 @@ for _ in range(2):
                   q_sp=sp, k_sp=sp, b_row=tile, b_col=tile, prefix=12, tau=dh ** -0.5, out=out)
 torch.cuda.synchronize()
 lib = _lib.load()
-buf = (ctypes.c_ulonglong * (64 * 16))()
-lib.zs_debug_glob_trace(buf, 64 * 16)
-a = np.array(buf, dtype=np.int64).reshape(64, 16)
+buf = (ctypes.c_ulonglong * (64 * 16 + 128))()
+lib.zs_debug_glob_trace(buf, 64 * 16 + 128)
+a = np.array(buf[:1024], dtype=np.int64).reshape(64, 16)
+t2 = np.array(buf[1024:], dtype=np.int64).reshape(16, 8)
 t0 = a[0, 6]
 names = ["c0_s", "c0_p", "wg0_start", "wg1_start", "wg0_done", "wg1_done", "q+bq", "S0", "S1", "S2", "S3", "S4", "S5", "S1_kful", "S1_ohful", "PV0_go"]
 print("item " + " ".join(f"{n:>9s}" for n in names))
 for k in range(12):
     print(f"{k:4d} " + " ".join(f"{(a[k, c] - t0) if a[k, c] else -1:9d}" for c in range(16)))
+
+print("item 5, per chunk: S' issued | sees S | P written | PV issued | k_full ok | oh_full ok | OH written | OH start")
+base = a[5, 6]
+for j in range(16):
+    if t2[j].any():
+        print(f"  chunk {j:2d} (WG {j % 2}?): " + " ".join(f"{(v - base) if v else -1:7d}" for v in t2[j]))
