@@ -65,7 +65,9 @@ def build(verbose: bool = False, force: bool = False, ptxas_verbose: bool = Fals
         obj = OBJ_DIR / (src.stem + ".o")
         objs.append(obj)
         if force or _stale(obj, [src, *headers]):
-            cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+            # ZS_BUILD_FLAGS: extra nvcc flags for diagnostics builds (e.g. -DZS_KERNEL_TRACE)
+            extra = os.environ.get("ZS_BUILD_FLAGS", "").split()
+            cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
             if ptxas_verbose:
                 cmd += ["-Xptxas", "-v"]
             jobs.append((src, cmd))
