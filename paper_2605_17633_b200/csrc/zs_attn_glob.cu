@@ -584,7 +584,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         tmem_ld32(o_oth + c0, b);
         tmem_ld_wait();
         if (valid) {
-          uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
+          uint4 o4[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             uint32_t v[8];
@@ -592,8 +592,10 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
             for (int e = 0; e < 8; ++e)  // a WG without chunks has a stale O: weight exactly 0
               v[e] = __float_as_uint((s_me != 0.f ? __uint_as_float(a[8 * q + e]) * s_me : 0.f) +
                                      (s_ot != 0.f ? __uint_as_float(b[8 * q + e]) * s_ot : 0.f));
-            d4[q] = scale_pack8(v, 1.f);
+            o4[q] = scale_pack8(v, 1.f);
           }
+          st_global_32B(dst + c0, o4[0], o4[1]);  // full 32-byte sectors
+          st_global_32B(dst + c0 + 16, o4[2], o4[3]);
         }
       }
       if constexpr (DH == 80) {
@@ -608,9 +610,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
             for (int e = 0; e < 16; ++e)
               v[e] = __float_as_uint((s_me != 0.f ? __uint_as_float(a[e]) * s_me : 0.f) +
                                      (s_ot != 0.f ? __uint_as_float(b[e]) * s_ot : 0.f));
-            uint4* d4 = reinterpret_cast<uint4*>(dst + 64);
-            d4[0] = scale_pack8(v, 1.f);
-            d4[1] = scale_pack8(v + 8, 1.f);
+            st_global_32B(dst + 64, scale_pack8(v, 1.f), scale_pack8(v + 8, 1.f));
           }
         }
       }

@@ -284,6 +284,12 @@ __device__ __forceinline__ float gelu_erf(float x) {
   const float erf_v = copysignf(erf_abs, x);
   return 0.5f * x * (1.0f + erf_v);
 }
+// 32-byte global store (sm_100 st.global.v8): one full sector per thread; dst 32-byte aligned
+__device__ __forceinline__ void st_global_32B(void* dst, uint4 lo, uint4 hi) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(lo.x), "r"(lo.y), "r"(lo.z),
+               "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
+               : "memory");
+}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);

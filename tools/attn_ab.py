@@ -1,0 +1,55 @@
+"""A/B timing of zs_stripe_attn_fwd from two library builds on the same box (interleaved rounds).
+
+    python tools/attn_ab.py [local|global] [B]   (needs _lib/libzstripe_b200_old.so next to the library)
+"""
+import ctypes
+import math
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2605_17633_b200 import _lib  # noqa: E402
+
+libs = {name: ctypes.CDLL(str(Path(_lib.LIB_PATH).parent / f)) for name, f in
+        [("new", "libzstripe_b200.so"), ("old", "libzstripe_b200_old.so")]}
+for l in libs.values():
+    l.zs_stripe_attn_fwd.argtypes = _lib.SIGNATURES["zs_stripe_attn_fwd"]
+kind = sys.argv[1] if len(sys.argv) > 1 else "local"
+B = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+H, dh = 16, 80
+S, w, tile = (196, 14, 32) if kind == "local" else (4096, 64, 128)
+U = B * 25 if kind == "local" else B
+C = H * dh
+p = math.floor(0.4 * (-(-S // tile)))
+qkv = torch.randn(U * S, 3 * C, device="cuda").bfloat16()
+bh = torch.randn(H, S, w, device="cuda") * 0.5
+bw = torch.randn(H, S, w, device="cuda") * 0.5
+sp = torch.argsort(torch.rand(U, S, device="cuda"), dim=1).int().contiguous()
+outs = {n: torch.empty(U * S, C, device="cuda", dtype=torch.bfloat16) for n in libs}
+st = torch.cuda.current_stream().cuda_stream
+
+
+def call(lib, out):
+    q = qkv
+    rc = lib.zs_stripe_attn_fwd(q.data_ptr(), q.data_ptr() + 2 * C, q.data_ptr() + 4 * C, 3 * C, 3 * C, 3 * C,
+                                S * 3 * C, S * 3 * C, U, H, S, S, dh, bh.data_ptr(), bw.data_ptr(), w, sp.data_ptr(),
+                                sp.data_ptr(), tile, tile, p, dh ** -0.5, out.data_ptr(), C, S * C, st)
+    assert rc == 0, rc
+
+
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+for rnd in range(3):
+    for name, lib in libs.items():
+        for _ in range(2):
+            call(lib, outs[name])
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(10):
+            call(lib, outs[name])
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"round {rnd} {kind} {name}: {e0.elapsed_time(e1) / 10:7.3f} ms", flush=True)
+d = (outs["new"].float() - outs["old"].float()).norm() / outs["old"].float().norm()
+print("rel diff new vs old:", d.item())
