@@ -115,6 +115,15 @@ ZS_API int zs_prefix_keep_rows(int U, int S, int K, const uint8_t* is_pad, int32
                         zs_stream_t stream);
 /* Generalisation: rows [begin, end) of every unit, pads skipped (the bypass set is
  * the span [K, S)).  rows holds U*(end-begin) entries. */
+/* Inverse of a row list: map[rows[i]] = i for i < n (n = min(*n_dev, n) when n_dev != NULL),
+ * every other entry of map[0..map_len) = -1.  Used for the compacted output rows of the
+ * window attention (zs_stripe_attn_fwd_rows) when window pad tokens are skipped. */
+ZS_API int zs_invert_rows(const int32_t* rows, long long n, const int32_t* n_dev, int32_t* map, long long map_len,
+                          zs_stream_t stream);
+/* dst[r, 0..ncol) = src_row[0..ncol) for every row r < rows with flag[r] != 0 (bf16, ncol % 8 == 0).
+ * Broadcasts the constant QKV row of the zero-padded window tokens (LN(0) = beta). */
+ZS_API int zs_fill_flagged_rows_bf16(void* dst, long long ld, const void* src_row, const uint8_t* flag,
+                                     long long rows, int ncol, zs_stream_t stream);
 ZS_API int zs_unit_span_rows(int U, int S, int begin, int end, const uint8_t* is_pad, int32_t* rows,
                              int32_t* unit_offsets, zs_stream_t stream);
 
@@ -159,6 +168,16 @@ ZS_API int zs_stripe_attn_fwd(const void* q, const void* k, const void* v, long 
                        int dh, const float* bh, const float* bw, int bias_w, const int32_t* q_sp,
                        const int32_t* k_sp, int b_row, int b_col, int prefix_tiles, float tau, void* out,
                        long long ldo, long long o_unit_stride, zs_stream_t stream);
+/* Same, with an output row map: row r of unit u goes to out row o_rows[u*sq + r] (head h at
+ * columns h*dh), or is not written when o_rows[...] < 0 (o_rows == NULL: the layout above).
+ * Lets a caller write only the query rows it keeps (e.g. skip SAM's window pad tokens,
+ * whose outputs the reference crops, encoder.py:366-368) into a compacted buffer. */
+ZS_API int zs_stripe_attn_fwd_rows(const void* q, const void* k, const void* v, long long ldq, long long ldk,
+                            long long ldv, long long q_unit_stride, long long kv_unit_stride, int units, int heads,
+                            int sq, int sk, int dh, const float* bh, const float* bw, int bias_w,
+                            const int32_t* q_sp, const int32_t* k_sp, int b_row, int b_col, int prefix_tiles,
+                            float tau, void* out, long long ldo, long long o_unit_stride, const int32_t* o_rows,
+                            zs_stream_t stream);
 
 /* ------------------------------------------------------------------- RC-MLP
  * Residual-consistency MLP on an fp32 residual stream x[rows, C] in place:

@@ -36,6 +36,10 @@ SIGNATURES: dict[str, list] = {
     "zs_gemm_bf16": [_i, _p, _ll, _p, _ll, _i, _i, _i, _p, _p, _ll, _p, _ll, _p, _p, _i, _p, _p],
     "zs_stripe_attn_fwd": [_p, _p, _p, _ll, _ll, _ll, _ll, _ll, _i, _i, _i, _i, _i, _p, _p, _i, _p, _p, _i, _i,
                            _i, _f, _p, _ll, _ll, _p],
+    "zs_stripe_attn_fwd_rows": [_p, _p, _p, _ll, _ll, _ll, _ll, _ll, _i, _i, _i, _i, _i, _p, _p, _i, _p, _p, _i, _i,
+                                _i, _f, _p, _ll, _ll, _p, _p],
+    "zs_invert_rows": [_p, _ll, _p, _p, _ll, _p],
+    "zs_fill_flagged_rows_bf16": [_p, _ll, _p, _p, _ll, _i, _p],
     "zs_rc_mlp_fwd": [_p, _ll, _p, _i, _p, _i, _i, _p, _p, _f, _p, _p, _p, _p, _i, _p, _i, _p, _p, _p],
     "zs_patchify": [_p, _i, _i, _i, _i, _i, _p, _p],
     "zs_im2col3x3": [_p, _i, _i, _i, _i, _p, _p],

@@ -52,6 +52,7 @@ constexpr int VST = 2;          // V ring stages
 struct Params {
   int units, heads, sq, sk, bias_w;
   long long ldo, o_unit_stride;
+  const int* o_rows;  // optional: output row of (unit, query row), -1 = not written
   const float* bh;
   const float* bw;
   const int* q_sp;
@@ -430,8 +431,14 @@ __global__ void __launch_bounds__(attn::kThreads, 1)
     };
     // O / ell -> bf16 -> global for a finished item (its last PV must be complete)
     auto epilogue = [&](int u_, int h_, int row_, float inv) {
-      const bool valid = row_ < P.sq;
-      __nv_bfloat16* dst = P.out + (long long)u_ * P.o_unit_stride + (long long)row_ * P.ldo + h_ * DH;
+      long long orow_off = (long long)u_ * P.o_unit_stride + (long long)row_ * P.ldo;
+      bool valid = row_ < P.sq;
+      if (valid && P.o_rows) {
+        const int m = P.o_rows[(long long)u_ * P.sq + row_];
+        valid = m >= 0;
+        orow_off = (long long)m * P.ldo;
+      }
+      __nv_bfloat16* dst = P.out + orow_off + h_ * DH;
       {
         uint32_t pr[32];
         tmem_ld32(o_addr, pr);
@@ -678,15 +685,15 @@ using namespace zs;
 int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                     long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
                     const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
-                    float tau, void* out, long long ldo, long long ous, cudaStream_t st);
+                    float tau, void* out, long long ldo, long long ous, const int* o_rows, cudaStream_t st);
 int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                      long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
                      const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
-                     float tau, void* out, long long ldo, long long ous, cudaStream_t st);
+                     float tau, void* out, long long ldo, long long ous, const int* o_rows, cudaStream_t st);
 int launch_attn_local(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                       long long qus, long long kvus, int units, int heads, int sq, int sk, int dh, const float* bh,
                       const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col,
-                      int prefix, float tau, void* out, long long ldo, long long ous, cudaStream_t st);
+                      int prefix, float tau, void* out, long long ldo, long long ous, const int* o_rows, cudaStream_t st);
 
 template <int DH, bool FAST>
 static int launch_attn(const CUtensorMap* m, attn::Params p, cudaStream_t st) {
@@ -765,6 +772,17 @@ extern "C" int zs_stripe_attn_fwd(const void* q, const void* k, const void* v, l
                                   const int32_t* q_sp, const int32_t* k_sp, int b_row, int b_col,
                                   int prefix_tiles, float tau, void* out, long long ldo, long long o_unit_stride,
                                   zs_stream_t stream) {
+  return zs_stripe_attn_fwd_rows(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, sk, dh, bh,
+                                 bw, bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride,
+                                 nullptr, stream);
+}
+
+extern "C" int zs_stripe_attn_fwd_rows(const void* q, const void* k, const void* v, long long ldq, long long ldk,
+                                       long long ldv, long long q_unit_stride, long long kv_unit_stride, int units,
+                                       int heads, int sq, int sk, int dh, const float* bh, const float* bw,
+                                       int bias_w, const int32_t* q_sp, const int32_t* k_sp, int b_row, int b_col,
+                                       int prefix_tiles, float tau, void* out, long long ldo,
+                                       long long o_unit_stride, const int32_t* o_rows, zs_stream_t stream) {
   if (units <= 0 || heads <= 0) return 0;
   if (!q || !k || !v || !bh || !bw || !q_sp || !k_sp || !out) return ZS_ERR_ARG;
   if (sq <= 0 || sk <= 0 || b_row <= 0 || b_col <= 0 || bias_w <= 0 || bias_w > 255) return ZS_ERR_SHAPE;
@@ -787,6 +805,7 @@ extern "C" int zs_stripe_attn_fwd(const void* q, const void* k, const void* v, l
   p.bias_w = bias_w;
   p.ldo = ldo;
   p.o_unit_stride = o_unit_stride;
+  p.o_rows = o_rows;
   p.bh = bh;
   p.bw = bw;
   p.q_sp = q_sp;
@@ -809,15 +828,17 @@ extern "C" int zs_stripe_attn_fwd(const void* q, const void* k, const void* v, l
     if (sq == sk && !getenv("ZS_ATTN_NO_WIN")) {
       const int rc = launch_attn_win(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, dh, bh,
                                      bw, bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride,
-                                     st);
+                                     o_rows, st);
       if (rc <= 0) return rc;
     }
     return launch_attn_local(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, sk, dh, bh, bw,
-                             bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride, st);
+                             bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride, o_rows,
+                             st);
   }
   if (sq == sk && !getenv("ZS_ATTN_NO_GLOB")) {  // 128x128 tiles: split-chunk TMEM-P kernel (zs_attn_glob.cu)
     const int rc = launch_attn_glob(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, dh, bh, bw,
-                                    bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride, st);
+                                    bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride, o_rows,
+                             st);
     if (rc <= 0) return rc;
   }
   if (dh == 64) return launch_attn_dh<64>(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, p, st);

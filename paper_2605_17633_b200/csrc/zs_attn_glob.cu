@@ -47,6 +47,7 @@ constexpr int OH_BYTES = 2 * BQ * 128;  // two 64-column SW128 slabs (e_ky | e_k
 struct Params {
   int units, heads, S, bias_w, T, prefix, items;
   long long ldo, o_unit_stride;
+  const int* o_rows;  // optional: output row of (unit, query row), -1 = not written
   const __half* btab;  // [heads, S, 128] fp16 rows: bh/tau in cols [0, w), bw/tau in [64, 64 + w)
   const int* q_sp;
   const int* k_sp;
@@ -574,8 +575,14 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       const float inv = 1.0f / (ell * a_me + lo * a_ot);
       const float s_me = a_me * inv, s_ot = a_ot * inv;
       tc_fence_after();
-      const bool valid = row < P.S;
-      __nv_bfloat16* dst = P.out + (long long)u * P.o_unit_stride + (long long)row * P.ldo + h * DH;
+      bool valid = row < P.S;
+      long long orow_off = (long long)u * P.o_unit_stride + (long long)row * P.ldo;
+      if (valid && P.o_rows) {
+        const int m = P.o_rows[(long long)u * P.S + row];
+        valid = m >= 0;
+        orow_off = (long long)m * P.ldo;
+      }
+      __nv_bfloat16* dst = P.out + orow_off + h * DH;
       // WG0: columns [0, 32) (+ [64, 80) when dh = 80), WG1: [32, 64)
       {
         const uint32_t c0 = w * 32;
@@ -637,7 +644,7 @@ using namespace zs;
 int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                      long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
                      const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
-                     float tau, void* out, long long ldo, long long ous, cudaStream_t st) {
+                     float tau, void* out, long long ldo, long long ous, const int* o_rows, cudaStream_t st) {
   using namespace attng;
   if (b_row != BQ || b_col != BQ || (dh != 64 && dh != 80) || S < 1 || bias_w > 64 || !(tau > 0.f)) return 1;
   Params p{};
@@ -652,6 +659,7 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
   p.items = (int)items;
   p.ldo = ldo;
   p.o_unit_stride = ous;
+  p.o_rows = o_rows;
   p.q_sp = q_sp;
   p.k_sp = k_sp;
   p.tau = tau;

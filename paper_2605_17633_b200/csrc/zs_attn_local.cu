@@ -32,6 +32,7 @@ constexpr uint32_t kTmemCols = 512;
 struct Params {
   int units, heads, sq, sk, bias_w;
   long long ldo, o_unit_stride;
+  const int* o_rows;  // optional: output row of (unit, query row), -1 = not written
   const float* bh;
   const float* bw;
   const int* q_sp;
@@ -428,8 +429,14 @@ __global__ void __launch_bounds__(attnl::kThreads, 1)
       mbar_wait(&o_full[X], (n - 1) & 1);
       tc_fence_after();
       const float inv = 1.0f / ell;
-      const bool valid = row < P.sq;
-      __nv_bfloat16* dst = P.out + (long long)u * P.o_unit_stride + (long long)row * P.ldo + h * DH;
+      bool valid = row < P.sq;
+      long long orow_off = (long long)u * P.o_unit_stride + (long long)row * P.ldo;
+      if (valid && P.o_rows) {
+        const int m = P.o_rows[(long long)u * P.sq + row];
+        valid = m >= 0;
+        orow_off = (long long)m * P.ldo;
+      }
+      __nv_bfloat16* dst = P.out + orow_off + h * DH;
 #pragma unroll
       for (int c0 = 0; c0 < 64; c0 += 32) {
         uint32_t pr[32];
@@ -468,7 +475,7 @@ using namespace zs;
 int launch_attn_local(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                       long long qus, long long kvus, int units, int heads, int sq, int sk, int dh, const float* bh,
                       const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col,
-                      int prefix, float tau, void* out, long long ldo, long long ous, cudaStream_t st) {
+                      int prefix, float tau, void* out, long long ldo, long long ous, const int* o_rows, cudaStream_t st) {
   attnl::Params p;
   p.units = units;
   p.heads = heads;
@@ -477,6 +484,7 @@ int launch_attn_local(const void* q, const void* k, const void* v, long long ldq
   p.bias_w = bias_w;
   p.ldo = ldo;
   p.o_unit_stride = ous;
+  p.o_rows = o_rows;
   p.bh = bh;
   p.bw = bw;
   p.q_sp = q_sp;

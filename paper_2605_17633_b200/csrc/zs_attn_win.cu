@@ -44,6 +44,7 @@ constexpr int kMaxRuns = 4;
 struct Params {
   int units, heads, S, bias_w, items, nt, nlw;
   long long ldo, o_unit_stride;
+  const int* o_rows;  // optional: output row of (unit, query row), -1 = not written
   const __half* btab;  // [heads, S, 32] fp16: bh/tau (cols 0..15), bw/tau (16..31), zero padded
   const __half* kb1;   // [S, 32] fp16 one-hot rows of every spatial key: e_{s/w} | e_{s%w}
   const int* q_sp;
@@ -452,14 +453,21 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
 
     auto epilogue = [&](int it, float inv) {
       const int u = it / P.heads, h = it % P.heads;
-      __nv_bfloat16* dst = P.out + (long long)u * P.o_unit_stride + (long long)row * P.ldo + h * DH;
-#pragma unroll
+      long long orow_off = (long long)u * P.o_unit_stride + (long long)row * P.ldo;
+      bool ok = valid;
+      if (ok && P.o_rows) {
+        const int m = P.o_rows[(long long)u * P.S + row];
+        ok = m >= 0;
+        orow_off = (long long)m * P.ldo;
+      }
+      __nv_bfloat16* dst = P.out + orow_off + h * DH;
       // 16-byte stores (measured faster here than 32-byte st.global.v8: tools/attn_ab.py)
+#pragma unroll
       for (int c0 = 0; c0 < 64; c0 += 32) {
         uint32_t pr[32];
         tmem_ld32(o_addr + c0, pr);
         tmem_ld_wait();
-        if (valid) {
+        if (ok) {
           uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
 #pragma unroll
           for (int j = 0; j < 4; ++j) d4[j] = scale_pack8(pr + 8 * j, inv);
@@ -469,7 +477,7 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         uint32_t p16[16];
         tmem_ld16(o_addr + 64, p16);
         tmem_ld_wait();
-        if (valid) {
+        if (ok) {
           uint4* d4 = reinterpret_cast<uint4*>(dst + 64);
           d4[0] = scale_pack8(p16, inv);
           d4[1] = scale_pack8(p16 + 8, inv);
@@ -593,7 +601,7 @@ static __half* win_btab(size_t elems) {
 int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                     long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
                     const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
-                    float tau, void* out, long long ldo, long long ous, cudaStream_t st) {
+                    float tau, void* out, long long ldo, long long ous, const int* o_rows, cudaStream_t st) {
   using namespace attnw;
   if (S <= 0 || S > 256 || (b_row % 32) || (b_col % 32) || (dh != 64 && dh != 80)) return 1;
   if (bias_w > 16 || bias_w * bias_w != S || !(tau > 0.f)) return 1;
@@ -606,6 +614,7 @@ int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, 
   p.nt = S > 128 ? 2 : 1;
   p.ldo = ldo;
   p.o_unit_stride = ous;
+  p.o_rows = o_rows;
   p.q_sp = q_sp;
   p.k_sp = k_sp;
   p.tau = tau;

@@ -303,6 +303,27 @@ __global__ void im2col3x3_kernel(const __nv_bfloat16* __restrict__ x, int B, int
   }
 }
 
+// map[rows[i]] = i for i < n (n = *n_dev when given); map must be pre-filled with -1
+__global__ void invert_rows_kernel(const int* __restrict__ rows, long long n, const int* __restrict__ n_dev,
+                                   int* __restrict__ map) {
+  long long nn = n;
+  if (n_dev) nn = min((long long)*n_dev, n);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nn; i += (long long)gridDim.x * blockDim.x)
+    map[rows[i]] = (int)i;
+}
+// dst[r, :] = src_row for every r with flag[r] != 0 (16-byte vectors): one warp per row, so
+// unflagged rows cost one byte read
+__global__ void fill_flagged_rows_kernel(uint4* __restrict__ dst, long long ld_vec, const uint4* __restrict__ src,
+                                         const uint8_t* __restrict__ flag, long long rows, int nvec) {
+  const int lane = threadIdx.x & 31;
+  const long long w0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long r = w0; r < rows; r += nw) {
+    if (!flag[r]) continue;
+    for (int v = lane; v < nvec; v += 32) dst[r * ld_vec + v] = __ldg(src + v);
+  }
+}
+
 }  // namespace zs
 
 // ================================================================== C ABI
@@ -409,5 +430,27 @@ extern "C" int zs_im2col3x3(const void* x, int B, int H, int W, int C, void* out
   if (C % 8 || (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out)) & 15) return ZS_ERR_ALIGN;
   im2col3x3_kernel<<<num_sms() * 8, 256, 0, S(stream)>>>(reinterpret_cast<const __nv_bfloat16*>(x), B, H, W, C,
                                                           reinterpret_cast<__nv_bfloat16*>(out));
+  return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
+}
+
+extern "C" int zs_invert_rows(const int32_t* rows, long long n, const int32_t* n_dev, int32_t* map, long long map_len,
+                              zs_stream_t stream) {
+  if (map_len <= 0) return 0;
+  if (!map || (n > 0 && !rows)) return ZS_ERR_ARG;
+  if (cudaMemsetAsync(map, 0xFF, (size_t)map_len * sizeof(int32_t), S(stream)) != cudaSuccess) return ZS_ERR_LAUNCH;
+  if (n > 0) invert_rows_kernel<<<grid_for_rows(n, 256), 256, 0, S(stream)>>>(rows, n, n_dev, map);
+  return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
+}
+
+extern "C" int zs_fill_flagged_rows_bf16(void* dst, long long ld, const void* src_row, const uint8_t* flag,
+                                         long long rows, int ncol, zs_stream_t stream) {
+  if (rows <= 0) return 0;
+  if (!dst || !src_row || !flag) return ZS_ERR_ARG;
+  if (ncol % 8 || ld % 8 || (reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src_row)) & 15)
+    return ZS_ERR_ALIGN;
+  const int nvec = ncol / 8;
+  fill_flagged_rows_kernel<<<num_sms() * 8, 256, 0, S(stream)>>>(reinterpret_cast<uint4*>(dst), ld / 8,
+                                                                 reinterpret_cast<const uint4*>(src_row), flag, rows,
+                                                                 nvec);
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }

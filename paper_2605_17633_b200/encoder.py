@@ -101,6 +101,7 @@ class StripeSortEncoder:
         self.morton_w = torch.as_tensor(morton_order_np(cfg.window, cfg.window)).to(**i32)
         self._ws: dict = {}
         self._ws_B = None
+        self._pad_rows: dict = {}
         self.has_local = "local" in cfg.layout
         self.has_global = "global" in cfg.layout
         self.tracer = NULL
@@ -161,11 +162,31 @@ class StripeSortEncoder:
         ws = self._ws
         if ws["mlp"].numel() < need:
             ws["mlp"] = torch.empty((need,), device=self.device, dtype=torch.bfloat16)
+        if self.has_local and "l_is_pad" in od.maps:
+            # window pad tokens: LN1 / QKV / proj run on the non-pad rows only (their outputs are
+            # cropped, encoder.py:366-368); the pads' K/V rows are the constant QKV row of LN(0)
+            U, S = B * self.nwin, self.S2
+            rows, offs = K.unit_span_rows(U, S, 0, S, od.maps["l_is_pad"], self.device)
+            sets["nonpad"] = dict(rows=rows, n=offs[U:U + 1], max=U * S,
+                                  omap=K.invert_rows(rows, U * S, n_dev=offs[U:U + 1]))
         return sets
+
+    def _pad_qkv_row(self, blk: BlockParams) -> torch.Tensor:
+        """QKV row of a zero-padded window token: LN(0) = beta exactly, so bf16(beta) @ Wqkv^T + b,
+        the same tcgen05 GEMM row the full-width QKV would compute.  Depends on the weights only:
+        computed once per block and cached."""
+        key = id(blk)
+        row = self._pad_rows.get(key)
+        if row is None:
+            C = self.cfg.d
+            hz = K.layernorm_rows(torch.zeros((1, C), device=self.device, dtype=torch.float32), blk.ln1_g, blk.ln1_b)
+            row = K.gemm(hz, blk.qkv_w, blk.qkv_b)
+            self._pad_rows[key] = row
+        return row
 
     # ------------------------------------------------------------ blocks
     def _block(self, blk: BlockParams, x: torch.Tensor, od: Orderings, B: int, r: float, rows: dict,
-               ws: dict) -> None:
+               ws: dict, nonpad: dict | None = None) -> None:
         cfg = self.cfg
         C, H, dh = cfg.d, cfg.heads, cfg.head_dim
         local = blk.kind == "local"
@@ -179,19 +200,35 @@ class StripeSortEncoder:
         xs = x[:R]
         tr = self.tracer
         w = blk.bh.shape[-1]
-        with tr.span("layernorm", bytes=R * C * 6):
-            h = K.layernorm_rows(xs, blk.ln1_g, blk.ln1_b, out=ws["h"][:R])
-        with tr.span("gemm_qkv", flops=2.0 * R * C * 3 * C, bytes=R * C * 2 + 3 * C * C * 2 + R * 3 * C * 2):
-            qkv = K.gemm(h, blk.qkv_w, blk.qkv_b, out=ws["qkv"][:R])
         E = attention_elements(S, tile, prefix)
-        with tr.span(f"attn_{blk.kind}", flops=4.0 * dh * E * U * H,
-                     bytes=U * H * 4 * S * dh * 2 + H * 2 * S * w * 4):
-            o = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], units=U, heads=H, sq=S, sk=S, dh=dh,
-                              bh=blk.bh, bw=blk.bw, q_sp=sig, k_sp=sig, b_row=tile, b_col=tile, prefix=prefix,
-                              tau=1.0 / math.sqrt(dh), out=ws["o"][:R])
-        with tr.span("gemm_proj", flops=2.0 * R * C * C, bytes=R * C * 2 + C * C * 2 + R * C * 8):
-            K.gemm(o, blk.proj_w, blk.proj_b, epi=K.EPI_F32_RESID, out=xs, res=xs,
-                   zero_rows=od.maps["l_is_pad"] if local else None)
+        if nonpad is not None:
+            # non-pad rows only (compacted), pad K/V rows = the constant row of LN(0) = beta
+            npr, nn, mx = nonpad["rows"], nonpad["n"], nonpad["max"]
+            with tr.span("layernorm", bytes=(nn, C * 6)):
+                h = K.layernorm_rows(xs, blk.ln1_g, blk.ln1_b, npr, out=ws["h"][:mx], n_dev=nn)
+            with tr.span("gemm_qkv", flops=(nn, 2.0 * C * 3 * C)):
+                qkv = K.gemm(h, blk.qkv_w, blk.qkv_b, out=ws["qkv"][:R], row_map=npr, m_dev=nn)
+                K.fill_flagged_rows(qkv, self._pad_qkv_row(blk), od.maps["l_is_pad"])
+            with tr.span(f"attn_{blk.kind}", flops=4.0 * dh * E * U * H,
+                         bytes=U * H * 4 * S * dh * 2 + H * 2 * S * w * 4):
+                o = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], units=U, heads=H, sq=S, sk=S, dh=dh,
+                                  bh=blk.bh, bw=blk.bw, q_sp=sig, k_sp=sig, b_row=tile, b_col=tile, prefix=prefix,
+                                  tau=1.0 / math.sqrt(dh), out=ws["o"][:R], o_rows=nonpad["omap"])
+            with tr.span("gemm_proj", flops=(nn, 2.0 * C * C)):
+                K.gemm(o[:mx], blk.proj_w, blk.proj_b, epi=K.EPI_F32_RESID, out=xs, res=xs, row_map=npr, m_dev=nn)
+        else:
+            with tr.span("layernorm", bytes=R * C * 6):
+                h = K.layernorm_rows(xs, blk.ln1_g, blk.ln1_b, out=ws["h"][:R])
+            with tr.span("gemm_qkv", flops=2.0 * R * C * 3 * C, bytes=R * C * 2 + 3 * C * C * 2 + R * 3 * C * 2):
+                qkv = K.gemm(h, blk.qkv_w, blk.qkv_b, out=ws["qkv"][:R])
+            with tr.span(f"attn_{blk.kind}", flops=4.0 * dh * E * U * H,
+                         bytes=U * H * 4 * S * dh * 2 + H * 2 * S * w * 4):
+                o = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], units=U, heads=H, sq=S, sk=S, dh=dh,
+                                  bh=blk.bh, bw=blk.bw, q_sp=sig, k_sp=sig, b_row=tile, b_col=tile, prefix=prefix,
+                                  tau=1.0 / math.sqrt(dh), out=ws["o"][:R])
+            with tr.span("gemm_proj", flops=2.0 * R * C * C, bytes=R * C * 2 + C * C * 2 + R * C * 8):
+                K.gemm(o, blk.proj_w, blk.proj_b, epi=K.EPI_F32_RESID, out=xs, res=xs,
+                       zero_rows=od.maps["l_is_pad"] if local else None)
         # RC-MLP (mlp.py:88-114): gather-LN of the kept rows -> fc1 + GELU -> fc2 + scatter-add residual
         nk = rows["n_keep"]
         mk = rows["max_keep"]
@@ -246,7 +283,7 @@ class StripeSortEncoder:
             kf = 1.0 if mode == "dense" else cfg.keep_fraction[bi]
             S = self.S2 if kind == "local" else self.HW
             Kc = RouterConfig(kf, cfg.bypass_mode).keep_count(S)
-            self._block(blk, cur, od, B, r, rows[(kind, Kc)], ws)
+            self._block(blk, cur, od, B, r, rows[(kind, Kc)], ws, rows.get("nonpad") if kind == "local" else None)
         if out is None:
             out = torch.empty((B * self.HW, cfg.d), device=self.device, dtype=torch.float32)
         with self.tracer.span("permute", bytes=out.numel() * 8):

@@ -248,9 +248,12 @@ def stripe_attn(
     out: torch.Tensor | None = None,
     q_unit_stride: int | None = None,
     kv_unit_stride: int | None = None,
+    o_rows: torch.Tensor | None = None,
 ) -> torch.Tensor:
     """Block-sparse stripe attention.  q/k/v are row-major views ``[units*S, ld]``
-    whose head ``h`` lives at columns ``h*dh``; ``out`` is ``[units*sq, heads*dh]``."""
+    whose head ``h`` lives at columns ``h*dh``; ``out`` is ``[units*sq, heads*dh]``, or, with
+    ``o_rows`` (int32 ``[units*sq]``), query row r of unit u goes to ``out[o_rows[u*sq + r]]``
+    and is skipped where ``o_rows < 0``."""
     for t, n in ((q, "q"), (k, "k"), (v, "v")):
         _need(t, torch.bfloat16, n)
         if t.stride(-1) != 1:
@@ -265,12 +268,46 @@ def stripe_attn(
     ldq, ldk, ldv = q.stride(0), k.stride(0), v.stride(0)
     qus = q_unit_stride if q_unit_stride is not None else sq * ldq
     kvus = kv_unit_stride if kv_unit_stride is not None else sk * ldk
-    _lib.call(
-        "zs_stripe_attn_fwd", _ptr(q), _ptr(k), _ptr(v), ldq, ldk, ldv, qus, kvus, units, heads, sq, sk, dh,
-        _ptr(bh.contiguous()), _ptr(bw.contiguous()), bias_w, _ptr(q_sp), _ptr(k_sp), b_row, b_col, prefix,
-        float(tau), _ptr(out), out.stride(0), sq * out.stride(0), _stream(),
-    )
+    if o_rows is None:
+        _lib.call(
+            "zs_stripe_attn_fwd", _ptr(q), _ptr(k), _ptr(v), ldq, ldk, ldv, qus, kvus, units, heads, sq, sk, dh,
+            _ptr(bh.contiguous()), _ptr(bw.contiguous()), bias_w, _ptr(q_sp), _ptr(k_sp), b_row, b_col, prefix,
+            float(tau), _ptr(out), out.stride(0), sq * out.stride(0), _stream(),
+        )
+    else:
+        _need(o_rows, torch.int32, "o_rows")
+        if o_rows.numel() < units * sq:
+            raise ValueError("o_rows must hold units*sq entries")
+        _lib.call(
+            "zs_stripe_attn_fwd_rows", _ptr(q), _ptr(k), _ptr(v), ldq, ldk, ldv, qus, kvus, units, heads, sq, sk, dh,
+            _ptr(bh.contiguous()), _ptr(bw.contiguous()), bias_w, _ptr(q_sp), _ptr(k_sp), b_row, b_col, prefix,
+            float(tau), _ptr(out), out.stride(0), sq * out.stride(0), _ptr(o_rows), _stream(),
+        )
     return out
+
+
+def invert_rows(rows: torch.Tensor, map_len: int, n_dev: torch.Tensor | None = None,
+                out: torch.Tensor | None = None) -> torch.Tensor:
+    """``map[rows[i]] = i`` (i < n, n from ``n_dev`` when given), -1 elsewhere; ``map`` has ``map_len`` entries."""
+    _need(rows, torch.int32, "rows")
+    if n_dev is not None:
+        _need(n_dev, torch.int32, "n_dev")
+    if out is None:
+        out = torch.empty(map_len, device=rows.device, dtype=torch.int32)
+    _lib.call("zs_invert_rows", _ptr(rows), rows.numel(), _ptr(n_dev), _ptr(out), map_len, _stream())
+    return out
+
+
+def fill_flagged_rows(dst: torch.Tensor, src_row: torch.Tensor, flag: torch.Tensor) -> torch.Tensor:
+    """``dst[r] = src_row`` for every row with ``flag[r] != 0`` (bf16 rows)."""
+    _need(dst, torch.bfloat16, "dst")
+    _need(src_row, torch.bfloat16, "src_row")
+    _need(flag, torch.uint8, "flag")
+    if dst.stride(1) != 1 or src_row.numel() < dst.shape[1] or flag.numel() < dst.shape[0]:
+        raise ValueError("fill_flagged_rows shapes")
+    _lib.call("zs_fill_flagged_rows_bf16", _ptr(dst), dst.stride(0), _ptr(src_row), _ptr(flag), dst.shape[0],
+              dst.shape[1], _stream())
+    return dst
 
 
 # ------------------------------------------------------------------ RC-MLP
