@@ -321,3 +321,34 @@ def test_im2col3x3_tap_major():
     ref = torch.stack([xp[:, :, ky:ky + 5, kx:kx + 7] for ky in range(3) for kx in range(3)], dim=-1)
     ref = ref.permute(0, 2, 3, 4, 1).reshape(2 * 5 * 7, 9 * 16)
     assert torch.equal(out.float(), ref)
+
+
+def test_attention_output_row_map_and_pad_helpers():
+    """zs_stripe_attn_fwd_rows writes row r of unit u to out[o_rows[u*S+r]] (skips -1) and equals the
+    plain layout otherwise; invert_rows / fill_flagged_rows (window pad-token skipping)."""
+    g = torch.Generator().manual_seed(21)
+    units, heads, S, dh, w = 6, 2, 196, 80, 14
+    C = heads * dh
+    qkv = torch.randn(units * S, 3 * C, generator=g).bfloat16().to(DEV)
+    bh = (0.5 * torch.randn(heads, S, w, generator=g)).to(DEV)
+    bw = (0.5 * torch.randn(heads, S, w, generator=g)).to(DEV)
+    sp = torch.stack([torch.randperm(S, generator=g) for _ in range(units)]).int().to(DEV)
+    kw = dict(units=units, heads=heads, sq=S, sk=S, dh=dh, bh=bh, bw=bw, q_sp=sp, k_sp=sp, b_row=32, b_col=32,
+              prefix=2, tau=dh ** -0.5)
+    full = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], **kw)
+    keep = (torch.rand(units * S, generator=g) < 0.8).to(DEV)
+    rows = keep.nonzero().flatten().int()
+    omap = K.invert_rows(rows, units * S)
+    assert torch.equal(omap[rows.long()].cpu(), torch.arange(rows.numel(), dtype=torch.int32))
+    assert bool((omap[~keep] == -1).all())
+    comp = torch.zeros(units * S, C, device=DEV, dtype=torch.bfloat16)
+    K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], out=comp, o_rows=omap, **kw)
+    n = rows.numel()
+    assert torch.equal(comp[:n], full[rows.long()])
+    assert bool((comp[n:] == 0).all())
+    dst = torch.zeros(10, 24, device=DEV, dtype=torch.bfloat16)
+    src = torch.randn(1, 24, generator=g).bfloat16().to(DEV)
+    flag = torch.tensor([0, 1, 1, 0, 0, 1, 0, 0, 0, 1], dtype=torch.uint8, device=DEV)
+    K.fill_flagged_rows(dst, src, flag)
+    assert torch.equal(dst[flag.bool()], src.expand(4, 24))
+    assert bool((dst[~flag.bool()] == 0).all())
