@@ -12,14 +12,15 @@ namespace zs {
 // ------------------------------------------------------------------ layernorm
 // Two-pass per-row LN with population variance (tensor.py:214-236):
 //   mean = sum(x)/C; c = x - mean; var = sum(c*c)/C; y = c * (1/sqrt(var+eps)) * g + b
-template <bool OUT_F32>
-__global__ void __launch_bounds__(256) ln_rows_kernel(const float* __restrict__ x, long long ldx,
+// MAXV = float4 columns per lane (C <= 128*MAXV); exact-width instantiations keep the row in
+// as few registers as possible (more rows in flight per SM)
+template <bool OUT_F32, int MAXV>
+__global__ void __launch_bounds__(256, MAXV <= 10 ? 3 : 2) ln_rows_kernel(const float* __restrict__ x, long long ldx,
                                                       const int* __restrict__ rows,
                                                       const int* __restrict__ out_rows, long long n,
                                                       const int* __restrict__ n_dev, int C,
                                                       const float* __restrict__ g, const float* __restrict__ b,
                                                       float eps, void* out, long long ldo) {
-  constexpr int MAXV = 16;  // C <= 2048
   long long nn = n;
   if (n_dev) nn = min((long long)*n_dev, n);
   const int lane = threadIdx.x & 31;
@@ -97,10 +98,24 @@ int launch_layernorm(const float* x, long long ldx, const int* rows, const int* 
   if (!x || !g || !b || !out) return ZS_ERR_ARG;
   if (C <= 0 || C % 4 || C > 2048 || ldx % 4 || (out_f32 ? ldo % 4 : ldo % 4)) return ZS_ERR_SHAPE;
   const int grid = grid_for_rows(n, 8);  // one warp per row, 8 rows per CTA
-  if (out_f32)
-    ln_rows_kernel<true><<<grid, 256, 0, st>>>(x, ldx, rows, out_rows, n, n_dev, C, g, b, eps, out, ldo);
-  else
-    ln_rows_kernel<false><<<grid, 256, 0, st>>>(x, ldx, rows, out_rows, n, n_dev, C, g, b, eps, out, ldo);
+  const int nv = (C / 4 + 31) / 32;      // float4 per lane
+#define ZS_LN(NV)                                                                                          \
+  if (out_f32)                                                                                             \
+    ln_rows_kernel<true, NV><<<grid, 256, 0, st>>>(x, ldx, rows, out_rows, n, n_dev, C, g, b, eps, out, ldo); \
+  else                                                                                                     \
+    ln_rows_kernel<false, NV><<<grid, 256, 0, st>>>(x, ldx, rows, out_rows, n, n_dev, C, g, b, eps, out, ldo);
+  if (nv <= 2) {
+    ZS_LN(2)
+  } else if (nv <= 6) {
+    ZS_LN(6)
+  } else if (nv <= 8) {
+    ZS_LN(8)
+  } else if (nv <= 10) {
+    ZS_LN(10)
+  } else {
+    ZS_LN(16)
+  }
+#undef ZS_LN
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }
 
