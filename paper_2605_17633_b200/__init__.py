@@ -18,6 +18,19 @@ from .config import (  # noqa: F401
     sam_config,
 )
 
+from .sptn import (  # noqa: F401  (reference tensor.py / grid.py file format)
+    SptnBadDtype,
+    SptnBadMagic,
+    SptnBadShape,
+    SptnBadVersion,
+    SptnError,
+    SptnTruncated,
+    permutation_read,
+    permutation_write,
+    tensor_read,
+    tensor_write,
+)
+
 __version__ = "0.1.0"
 
 _API = {

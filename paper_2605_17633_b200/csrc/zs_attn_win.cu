@@ -422,7 +422,13 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
             const int sp = __shfl_sync(0xffffffffu, idx[i], rl);
             if (r < nrows) {
               uint8_t* dst = slab + sw32_off(r, c & 1);
-              if (sp >= 0) cp_async16(dst, tab + (long long)sp * 32 + c * 8);
+#ifdef ZS_WIN_NOGATHER
+              if (false) {
+#else
+              if (sp >= 0) {
+#endif
+                cp_async16(dst, tab + (long long)sp * 32 + c * 8);
+              }
               else *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);  // key rows past S
             }
           }
@@ -467,7 +473,11 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         uint32_t pr[32];
         tmem_ld32(o_addr + c0, pr);
         tmem_ld_wait();
+#ifdef ZS_WIN_NOSTORE
+        if (ok && pr[0] == 0x7fffffffu) {
+#else
         if (ok) {
+#endif
           uint4* d4 = reinterpret_cast<uint4*>(dst + c0);
 #pragma unroll
           for (int j = 0; j < 4; ++j) d4[j] = scale_pack8(pr + 8 * j, inv);
@@ -477,7 +487,11 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         uint32_t p16[16];
         tmem_ld16(o_addr + 64, p16);
         tmem_ld_wait();
+#ifdef ZS_WIN_NOSTORE
+        if (ok && p16[0] == 0x7fffffffu) {
+#else
         if (ok) {
+#endif
           uint4* d4 = reinterpret_cast<uint4*>(dst + 64);
           d4[0] = scale_pack8(p16, inv);
           d4[1] = scale_pack8(p16 + 8, inv);

@@ -150,8 +150,21 @@ def config1_blocks():
     save("config1_blocks", **out)
 
 
+def sptn_files():
+    """SPTN files written by the reference (tensor.py:65-84, grid.py:122-127) for the reader/writer gate."""
+    d = OUT / "sptn"
+    d.mkdir(exist_ok=True)
+    Z.tensor_write(np.array([3.0], dtype=np.float32), d / "scalar.sptn")
+    Z.tensor_write(Z.Rng(7).normal((3, 5, 4)), d / "rank3.sptn")
+    Z.tensor_write(Z.sobel_magnitude(Z.Rng(1).normal((6, 10, 8))).values, d / "sobel_6x10.sptn")
+    Z.permutation_write(Z.morton_order(Z.GridShape(6, 10)), d / "morton_6x10.sptn")
+    print("wrote", sorted(p.name for p in d.iterdir()))
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["grid", "c1orders", "attn", "mlp", "enc", "c1blocks"]
+    which = sys.argv[1:] or ["grid", "c1orders", "attn", "mlp", "enc", "c1blocks", "sptn"]
+    if "sptn" in which:
+        sptn_files()
     if "grid" in which:
         grid_and_orders()
     if "c1orders" in which:
