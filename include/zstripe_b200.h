@@ -16,6 +16,7 @@
 #ifndef ZSTRIPE_B200_H_
 #define ZSTRIPE_B200_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -178,6 +179,42 @@ ZS_API int zs_stripe_attn_fwd_rows(const void* q, const void* k, const void* v, 
                             const int32_t* q_sp, const int32_t* k_sp, int b_row, int b_col, int prefix_tiles,
                             float tau, void* out, long long ldo, long long o_unit_stride, const int32_t* o_rows,
                             zs_stream_t stream);
+
+/* Same as zs_stripe_attn_fwd_rows with one bias table pair PER UNIT: bh / bw of unit u start at
+ * u * bias_unit_stride floats (each [heads, S, w], spatial-position rows as above).  The
+ * reference's BiasTables (attention.py:28-55) generalised to per-window / per-image tables. */
+ZS_API int zs_stripe_attn_fwd_unit_bias(const void* q, const void* k, const void* v, long long ldq, long long ldk,
+                                        long long ldv, long long q_unit_stride, long long kv_unit_stride, int units,
+                                        int heads, int sq, int sk, int dh, const float* bh, const float* bw,
+                                        long long bias_unit_stride, int bias_w, const int32_t* q_sp,
+                                        const int32_t* k_sp, int b_row, int b_col, int prefix_tiles, float tau,
+                                        void* out, long long ldo, long long o_unit_stride, const int32_t* o_rows,
+                                        zs_stream_t stream);
+
+/* ------------------------------------------------ SAM decomposed relative position (q-dependent)
+ * SAM's add_decomposed_rel_pos (not in the reference, whose bias tables are static: SURVEY §8(f)
+ * row 2).  For every unit u, head h and query row r (spatial s = q_sp[u, r] = (qy, qx) of a
+ * w x w grid, S == w * w):
+ *   bh[u, h, s, ky] = q[u, r, h*dh : (h+1)*dh] . rel_pos_h[qy - ky + w - 1, :]
+ *   bw[u, h, s, kx] = q[u, r, h*dh : (h+1)*dh] . rel_pos_w[qx - kx + w - 1, :]
+ * rel_pos_h / rel_pos_w: fp32 [2w - 1, dh] (shared by the heads); q bf16 rows as in
+ * zs_stripe_attn_fwd (unscaled).  bf16 tensor-core products with fp32 accumulation.
+ * ws: >= zs_relpos_ws_bytes(...) bytes, 256-byte aligned (zs_relpos_bias needs the first
+ * 32 KB only).  w <= 64, dh 64 / 80. */
+ZS_API size_t zs_relpos_ws_bytes(int units, int heads, int S, int dh, int bias_w);
+ZS_API int zs_relpos_bias(const void* q, long long ldq, long long q_unit_stride, int units, int heads, int S, int dh,
+                          int bias_w, const float* rel_pos_h, const float* rel_pos_w, const int32_t* q_sp, float* bh,
+                          float* bw, void* ws, size_t ws_bytes, zs_stream_t stream);
+/* Stripe-sort attention with SAM's q-dependent decomposed bias: the bias operand rows are
+ * computed by a tcgen05 GEMM (q . [rel_pos_h; rel_pos_w]^T) straight into the attention kernels'
+ * fp16 operand layout (no fp32 table round trip); other arguments as zs_stripe_attn_fwd_rows
+ * with sq == sk == S. */
+ZS_API int zs_stripe_attn_fwd_relpos(const void* q, const void* k, const void* v, long long ldq, long long ldk,
+                                     long long ldv, long long q_unit_stride, long long kv_unit_stride, int units,
+                                     int heads, int S, int dh, const float* rel_pos_h, const float* rel_pos_w,
+                                     int bias_w, const int32_t* q_sp, const int32_t* k_sp, int b_row, int b_col,
+                                     int prefix_tiles, float tau, void* out, long long ldo, long long o_unit_stride,
+                                     const int32_t* o_rows, void* ws, size_t ws_bytes, zs_stream_t stream);
 
 /* ------------------------------------------------------------------- RC-MLP
  * Residual-consistency MLP on an fp32 residual stream x[rows, C] in place:

@@ -19,6 +19,7 @@ _p = C.c_void_p
 _i = C.c_int
 _ll = C.c_longlong
 _f = C.c_float
+_sz = C.c_size_t
 
 # name -> argtypes (restype is c_int unless noted)
 SIGNATURES: dict[str, list] = {
@@ -38,6 +39,12 @@ SIGNATURES: dict[str, list] = {
                            _i, _f, _p, _ll, _ll, _p],
     "zs_stripe_attn_fwd_rows": [_p, _p, _p, _ll, _ll, _ll, _ll, _ll, _i, _i, _i, _i, _i, _p, _p, _i, _p, _p, _i, _i,
                                 _i, _f, _p, _ll, _ll, _p, _p],
+    "zs_stripe_attn_fwd_unit_bias": [_p, _p, _p, _ll, _ll, _ll, _ll, _ll, _i, _i, _i, _i, _i, _p, _p, _ll, _i, _p,
+                                     _p, _i, _i, _i, _f, _p, _ll, _ll, _p, _p],
+    "zs_relpos_ws_bytes": [_i, _i, _i, _i, _i],  # returns size_t
+    "zs_relpos_bias": [_p, _ll, _ll, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _sz, _p],
+    "zs_stripe_attn_fwd_relpos": [_p, _p, _p, _ll, _ll, _ll, _ll, _ll, _i, _i, _i, _i, _p, _p, _i, _p, _p, _i, _i, _i,
+                                  _f, _p, _ll, _ll, _p, _p, _sz, _p],
     "zs_invert_rows": [_p, _ll, _p, _p, _ll, _p],
     "zs_fill_flagged_rows_bf16": [_p, _ll, _p, _p, _ll, _i, _p],
     "zs_rc_mlp_fwd": [_p, _ll, _p, _i, _p, _i, _i, _p, _p, _f, _p, _p, _p, _p, _i, _p, _i, _p, _p, _p],
@@ -65,6 +72,7 @@ def load() -> C.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = _i
+    lib.zs_relpos_ws_bytes.restype = _sz
     _lib = lib
     return lib
 
@@ -79,7 +87,8 @@ def status_string(rc: int) -> str:
 
 # kernel launches issued per successful ABI call (composites launch several)
 LAUNCHES_PER_CALL = {"zs_rc_mlp_fwd": 3, "zs_unit_span_rows": 3, "zs_prefix_keep_rows": 3, "zs_layout_maps": 3,
-                     "zs_abi_version": 0}
+                     "zs_abi_version": 0, "zs_relpos_ws_bytes": 0, "zs_relpos_bias": 2,
+                     "zs_stripe_attn_fwd_relpos": 4}
 launch_count = 0
 
 

@@ -33,6 +33,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cuda_fp16.h>
+
 #include "zs_common.cuh"
 #include "zs_host.h"
 
@@ -54,6 +56,7 @@ struct Params {
   long long ldo, o_unit_stride;
   const int* o_rows;  // optional: output row of (unit, query row), -1 = not written
   const float* bh;
+  long long bias_us;  // floats between the bh / bw tables of consecutive units (0: shared)
   const float* bw;
   const int* q_sp;
   const int* k_sp;
@@ -425,7 +428,7 @@ __global__ void __launch_bounds__(attn::kThreads, 1)
     auto stage_bias = [&](int u_, int h_, int mb_, int buf) {
       const int rw = mb_ * BQ + r;
       const int sp = P.q_sp[(long long)u_ * P.sq + (rw < P.sq ? rw : P.sq - 1)];
-      const float* src = (half ? P.bw : P.bh) + ((long long)h_ * P.sq + sp) * P.bias_w;
+      const float* src = (half ? P.bw : P.bh) + (long long)u_ * P.bias_us + ((long long)h_ * P.sq + sp) * P.bias_w;
       float* dst = bias_base + buf * bias_stride + half * BQ * W1 + r * W1;
       for (int j = 0; j < P.bias_w; ++j) cp_async4(dst + j, src + j);
     };
@@ -685,15 +688,24 @@ using namespace zs;
 int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                     long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
                     const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
-                    float tau, void* out, long long ldo, long long ous, const int* o_rows, cudaStream_t st);
+                    float tau, void* out, long long ldo, long long ous, const int* o_rows, long long bias_us,
+                    const __half* btab_ext, long long btab_us, cudaStream_t st);
 int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                      long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
                      const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
-                     float tau, void* out, long long ldo, long long ous, const int* o_rows, cudaStream_t st);
+                     float tau, void* out, long long ldo, long long ous, const int* o_rows, long long bias_us,
+                     const __half* btab_ext, long long btab_us, cudaStream_t st);
 int launch_attn_local(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                       long long qus, long long kvus, int units, int heads, int sq, int sk, int dh, const float* bh,
                       const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col,
-                      int prefix, float tau, void* out, long long ldo, long long ous, const int* o_rows, cudaStream_t st);
+                      int prefix, float tau, void* out, long long ldo, long long ous, const int* o_rows,
+                      long long bias_us, cudaStream_t st);
+namespace zs {
+size_t relpos_r_bytes(int dh, int w);
+int launch_relpos(const void* q, long long ldq, long long qus, int units, int heads, int S, int dh, int w,
+                  const float* rel_h, const float* rel_w, const int* q_sp, float tau, int mode, __half* btab,
+                  long long btab_us, float* bh, float* bw, void* ws, cudaStream_t st);
+}  // namespace zs
 
 template <int DH, bool FAST>
 static int launch_attn(const CUtensorMap* m, attn::Params p, cudaStream_t st) {
@@ -766,27 +778,20 @@ static int launch_attn_dh(const void* q, const void* k, const void* v, long long
   return launch_attn<DH, false>(m, p, st);
 }
 
-extern "C" int zs_stripe_attn_fwd(const void* q, const void* k, const void* v, long long ldq, long long ldk,
-                                  long long ldv, long long q_unit_stride, long long kv_unit_stride, int units,
-                                  int heads, int sq, int sk, int dh, const float* bh, const float* bw, int bias_w,
-                                  const int32_t* q_sp, const int32_t* k_sp, int b_row, int b_col,
-                                  int prefix_tiles, float tau, void* out, long long ldo, long long o_unit_stride,
-                                  zs_stream_t stream) {
-  return zs_stripe_attn_fwd_rows(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, sk, dh, bh,
-                                 bw, bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride,
-                                 nullptr, stream);
-}
-
-extern "C" int zs_stripe_attn_fwd_rows(const void* q, const void* k, const void* v, long long ldq, long long ldk,
-                                       long long ldv, long long q_unit_stride, long long kv_unit_stride, int units,
-                                       int heads, int sq, int sk, int dh, const float* bh, const float* bw,
-                                       int bias_w, const int32_t* q_sp, const int32_t* k_sp, int b_row, int b_col,
-                                       int prefix_tiles, float tau, void* out, long long ldo,
-                                       long long o_unit_stride, const int32_t* o_rows, zs_stream_t stream) {
+// Validation + kernel choice shared by every public entry.  bias_us: floats between the bh / bw
+// tables of consecutive units (0 = one [heads, S, w] table for all).  btab_ext: precomputed fp16
+// operand rows (zs_relpos.cu mode 0) for the window / global kernels; with it only those two are
+// tried and 1 is returned when neither accepts the shape.
+static int attn_dispatch(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
+                         long long q_unit_stride, long long kv_unit_stride, int units, int heads, int sq, int sk,
+                         int dh, const float* bh, const float* bw, long long bias_us, int bias_w, const int32_t* q_sp,
+                         const int32_t* k_sp, int b_row, int b_col, int prefix_tiles, float tau, void* out,
+                         long long ldo, long long o_unit_stride, const int32_t* o_rows, const __half* btab_ext,
+                         long long btab_us, cudaStream_t st) {
   if (units <= 0 || heads <= 0) return 0;
-  if (!q || !k || !v || !bh || !bw || !q_sp || !k_sp || !out) return ZS_ERR_ARG;
+  if (!q || !k || !v || ((!bh || !bw) && !btab_ext) || !q_sp || !k_sp || !out) return ZS_ERR_ARG;
   if (sq <= 0 || sk <= 0 || b_row <= 0 || b_col <= 0 || bias_w <= 0 || bias_w > 255) return ZS_ERR_SHAPE;
-  if (bias_w * bias_w != sk) return ZS_ERR_SHAPE;
+  if (bias_w * bias_w != sk || bias_us < 0) return ZS_ERR_SHAPE;
   if (dh != 64 && dh != 80) return ZS_ERR_SHAPE;
   const int tc = (sk + b_col - 1) / b_col;
   if (prefix_tiles < 0 || prefix_tiles > tc) return ZS_ERR_SHAPE;
@@ -797,6 +802,27 @@ extern "C" int zs_stripe_attn_fwd_rows(const void* q, const void* k, const void*
   const long long nmb = (sq + attn::BQ - 1) / attn::BQ;
   const long long items = nmb * heads * (long long)units;
   if (items > 0x7FFFFFFF) return ZS_ERR_SHAPE;
+  if (sq <= 256 && sk <= 256 && !getenv("ZS_ATTN_FORCE_GENERIC")) {
+    // windows: one-pass TMEM-P kernel (zs_attn_win.cu) when the schedule fits its envelope,
+    // else the ping-pong window kernel (zs_attn_local.cu)
+    if (sq == sk && !getenv("ZS_ATTN_NO_WIN")) {
+      const int rc = launch_attn_win(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, dh, bh,
+                                     bw, bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride,
+                                     o_rows, bias_us, btab_ext, btab_us, st);
+      if (rc <= 0 || btab_ext) return rc;
+    }
+    if (btab_ext) return 1;
+    return launch_attn_local(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, sk, dh, bh, bw,
+                             bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride, o_rows,
+                             bias_us, st);
+  }
+  if (sq == sk && !getenv("ZS_ATTN_NO_GLOB")) {  // 128x128 tiles: split-chunk TMEM-P kernel (zs_attn_glob.cu)
+    const int rc = launch_attn_glob(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, dh, bh, bw,
+                                    bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride, o_rows,
+                                    bias_us, btab_ext, btab_us, st);
+    if (rc <= 0 || btab_ext) return rc;
+  }
+  if (btab_ext) return 1;
   attn::Params p;
   p.units = units;
   p.heads = heads;
@@ -808,6 +834,7 @@ extern "C" int zs_stripe_attn_fwd_rows(const void* q, const void* k, const void*
   p.o_rows = o_rows;
   p.bh = bh;
   p.bw = bw;
+  p.bias_us = bias_us;
   p.q_sp = q_sp;
   p.k_sp = k_sp;
   p.b_row = b_row;
@@ -821,26 +848,109 @@ extern "C" int zs_stripe_attn_fwd_rows(const void* q, const void* k, const void*
   p.bias_bufs = 1;
   p.off_bias = 0;
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (sq <= 256 && sk <= 256 && !getenv("ZS_ATTN_FORCE_GENERIC")) {
-    // windows: one-pass TMEM-P kernel (zs_attn_win.cu) when the schedule fits its envelope,
-    // else the ping-pong window kernel (zs_attn_local.cu)
-    if (sq == sk && !getenv("ZS_ATTN_NO_WIN")) {
-      const int rc = launch_attn_win(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, dh, bh,
-                                     bw, bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride,
-                                     o_rows, st);
-      if (rc <= 0) return rc;
-    }
-    return launch_attn_local(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, sk, dh, bh, bw,
-                             bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride, o_rows,
-                             st);
-  }
-  if (sq == sk && !getenv("ZS_ATTN_NO_GLOB")) {  // 128x128 tiles: split-chunk TMEM-P kernel (zs_attn_glob.cu)
-    const int rc = launch_attn_glob(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, dh, bh, bw,
-                                    bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride, o_rows,
-                             st);
-    if (rc <= 0) return rc;
-  }
   if (dh == 64) return launch_attn_dh<64>(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, p, st);
   return launch_attn_dh<80>(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, p, st);
+}
+
+extern "C" int zs_stripe_attn_fwd(const void* q, const void* k, const void* v, long long ldq, long long ldk,
+                                  long long ldv, long long q_unit_stride, long long kv_unit_stride, int units,
+                                  int heads, int sq, int sk, int dh, const float* bh, const float* bw, int bias_w,
+                                  const int32_t* q_sp, const int32_t* k_sp, int b_row, int b_col,
+                                  int prefix_tiles, float tau, void* out, long long ldo, long long o_unit_stride,
+                                  zs_stream_t stream) {
+  return attn_dispatch(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, sk, dh, bh, bw, 0,
+                       bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride, nullptr, nullptr,
+                       0, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int zs_stripe_attn_fwd_rows(const void* q, const void* k, const void* v, long long ldq, long long ldk,
+                                       long long ldv, long long q_unit_stride, long long kv_unit_stride, int units,
+                                       int heads, int sq, int sk, int dh, const float* bh, const float* bw,
+                                       int bias_w, const int32_t* q_sp, const int32_t* k_sp, int b_row, int b_col,
+                                       int prefix_tiles, float tau, void* out, long long ldo,
+                                       long long o_unit_stride, const int32_t* o_rows, zs_stream_t stream) {
+  return attn_dispatch(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, sk, dh, bh, bw, 0,
+                       bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride, o_rows, nullptr,
+                       0, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int zs_stripe_attn_fwd_unit_bias(const void* q, const void* k, const void* v, long long ldq, long long ldk,
+                                            long long ldv, long long q_unit_stride, long long kv_unit_stride,
+                                            int units, int heads, int sq, int sk, int dh, const float* bh,
+                                            const float* bw, long long bias_unit_stride, int bias_w,
+                                            const int32_t* q_sp, const int32_t* k_sp, int b_row, int b_col,
+                                            int prefix_tiles, float tau, void* out, long long ldo,
+                                            long long o_unit_stride, const int32_t* o_rows, zs_stream_t stream) {
+  return attn_dispatch(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, sk, dh, bh, bw,
+                       bias_unit_stride, bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride,
+                       o_rows, nullptr, 0, reinterpret_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------- SAM relative-position mode
+static size_t relpos_tables_bytes(int units, int heads, int S, int bias_w) {
+  const size_t w16 = 2 * (size_t)((bias_w + 15) & ~15);
+  const size_t op = (size_t)units * heads * S * w16 * 2;           // fp16 operand rows
+  const size_t f32 = 2 * (size_t)units * heads * S * bias_w * 4;   // fp32 bh, bw (fallback kernels)
+  return ((op > f32 ? op : f32) + 255) & ~(size_t)255;
+}
+
+extern "C" size_t zs_relpos_ws_bytes(int units, int heads, int S, int dh, int bias_w) {
+  if (units <= 0 || heads <= 0 || bias_w <= 0 || bias_w > 64 || (dh != 64 && dh != 80)) return 0;
+  return relpos_r_bytes(dh, bias_w) + relpos_tables_bytes(units, heads, S, bias_w);
+}
+
+extern "C" int zs_relpos_bias(const void* q, long long ldq, long long q_unit_stride, int units, int heads, int S,
+                              int dh, int bias_w, const float* rel_pos_h, const float* rel_pos_w,
+                              const int32_t* q_sp, float* bh, float* bw, void* ws, size_t ws_bytes,
+                              zs_stream_t stream) {
+  if (units <= 0 || heads <= 0) return 0;
+  if (!q || !rel_pos_h || !rel_pos_w || !q_sp || !bh || !bw || !ws) return ZS_ERR_ARG;
+  if ((dh != 64 && dh != 80) || bias_w <= 0 || bias_w > 64 || bias_w * bias_w != S) return ZS_ERR_SHAPE;
+  if (ws_bytes < relpos_r_bytes(dh, bias_w)) return ZS_ERR_SHAPE;
+  if (((ldq | q_unit_stride) & 7) || (reinterpret_cast<uintptr_t>(q) & 15) || (reinterpret_cast<uintptr_t>(ws) & 255))
+    return ZS_ERR_ALIGN;
+  const int rc = launch_relpos(q, ldq, q_unit_stride, units, heads, S, dh, bias_w, rel_pos_h, rel_pos_w, q_sp, 1.0f, 1,
+                               nullptr, 0, bh, bw, ws, reinterpret_cast<cudaStream_t>(stream));
+  return rc == 1 ? ZS_ERR_SHAPE : rc;
+}
+
+extern "C" int zs_stripe_attn_fwd_relpos(const void* q, const void* k, const void* v, long long ldq, long long ldk,
+                                         long long ldv, long long q_unit_stride, long long kv_unit_stride, int units,
+                                         int heads, int S, int dh, const float* rel_pos_h, const float* rel_pos_w,
+                                         int bias_w, const int32_t* q_sp, const int32_t* k_sp, int b_row, int b_col,
+                                         int prefix_tiles, float tau, void* out, long long ldo,
+                                         long long o_unit_stride, const int32_t* o_rows, void* ws, size_t ws_bytes,
+                                         zs_stream_t stream) {
+  if (units <= 0 || heads <= 0) return 0;
+  if (!rel_pos_h || !rel_pos_w || !ws) return ZS_ERR_ARG;
+  if ((dh != 64 && dh != 80) || bias_w <= 0 || bias_w > 64 || bias_w * bias_w != S) return ZS_ERR_SHAPE;
+  if (ws_bytes < zs_relpos_ws_bytes(units, heads, S, dh, bias_w)) return ZS_ERR_SHAPE;
+  if (reinterpret_cast<uintptr_t>(ws) & 255) return ZS_ERR_ALIGN;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* tables = reinterpret_cast<uint8_t*>(ws) + relpos_r_bytes(dh, bias_w);
+  // fast kernels: fp16 operand rows straight from the relpos GEMM epilogue
+  const bool fast_shape = (S <= 256) ? (b_row % 32 == 0 && b_col % 32 == 0) : (b_row == 128 && b_col == 128);
+  if (fast_shape) {
+    const long long w16 = 2 * ((bias_w + 15) & ~15);
+    const long long us = (long long)heads * S * w16;
+    __half* btab = reinterpret_cast<__half*>(tables);
+    int rc = launch_relpos(q, ldq, q_unit_stride, units, heads, S, dh, bias_w, rel_pos_h, rel_pos_w, q_sp, tau, 0,
+                           btab, us, nullptr, nullptr, ws, st);
+    if (rc < 0) return rc;
+    if (rc == 0) {
+      rc = attn_dispatch(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, S, S, dh, nullptr,
+                         nullptr, 0, bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride,
+                         o_rows, btab, us, st);
+      if (rc <= 0) return rc;
+    }
+  }
+  // any other schedule: fp32 per-unit tables, then the kernels that read them
+  float* bh = reinterpret_cast<float*>(tables);
+  float* bw = bh + (size_t)units * heads * S * bias_w;
+  const int rc = zs_relpos_bias(q, ldq, q_unit_stride, units, heads, S, dh, bias_w, rel_pos_h, rel_pos_w, q_sp, bh, bw,
+                                ws, relpos_r_bytes(dh, bias_w), stream);
+  if (rc) return rc;
+  return attn_dispatch(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, S, S, dh, bh, bw,
+                       (long long)heads * S * bias_w, bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo,
+                       o_unit_stride, o_rows, nullptr, 0, st);
 }

@@ -49,6 +49,7 @@ struct Params {
   long long ldo, o_unit_stride;
   const int* o_rows;  // optional: output row of (unit, query row), -1 = not written
   const __half* btab;  // [heads, S, 128] fp16 rows: bh/tau in cols [0, w), bw/tau in [64, 64 + w)
+  long long btab_us;   // halves between the tables of consecutive units (0: one table for all)
   const int* q_sp;
   const int* k_sp;
   float tau;
@@ -449,7 +450,8 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       const int row2 = i2 * BQ + r;
       if (row2 < P.S) {
         const int sp = __ldg(P.q_sp + (long long)u2 * P.S + row2);
-        const uint4* src = reinterpret_cast<const uint4*>(P.btab + ((long long)h2 * P.S + sp) * 128 + w * 64);
+        const uint4* src = reinterpret_cast<const uint4*>(P.btab + (long long)u2 * P.btab_us +
+                                                      ((long long)h2 * P.S + sp) * 128 + w * 64);
 #pragma unroll
         for (int q = 0; q < 8; ++q) x[q] = __ldg(src + q);
       } else {
@@ -506,10 +508,13 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
           m1 = fmaxf(m1, __uint_as_float(sr[jj + 1]));
         }
         const float mx = tau * fmaxf(m0, m1);  // max logit (tau > 0)
-        // lazy rescale: the reference max moves only past the threshold
+        // lazy rescale: the reference max moves only past the threshold.  The O rescale is a
+        // warp-wide TMEM round trip (tcgen05.ld / st are .sync.aligned): taken when ANY row of
+        // the warp moves its reference, with alpha = 1 for the rows that do not
         float alpha = 1.f;
-        if (mx > m_ref + kThr || (m_ref == -INFINITY && mx > -INFINITY)) {
-          alpha = (m_ref == -INFINITY) ? 0.f : ex2((m_ref - mx) * L2E);
+        const bool upd = mx > m_ref + kThr || (m_ref == -INFINITY && mx > -INFINITY);
+        if (upd) alpha = (m_ref == -INFINITY) ? 0.f : ex2((m_ref - mx) * L2E);
+        if (__any_sync(0xffffffffu, upd)) {
           if (mine > 0) {
             // previous PV into O_w must have completed before O_w is rescaled
             mbar_wait(&o_full[w], (nsw - 1) & 1);
@@ -534,7 +539,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
               tmem_st16(o_addr + 64, p16);
             }
           }
-          m_ref = mx;
+          if (upd) m_ref = mx;
         }
         const float mc = (m_ref == -INFINITY) ? 0.f : m_ref * L2E;
         float r0 = 0.f, r1 = 0.f;
@@ -644,7 +649,8 @@ using namespace zs;
 int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                      long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
                      const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
-                     float tau, void* out, long long ldo, long long ous, const int* o_rows, cudaStream_t st) {
+                     float tau, void* out, long long ldo, long long ous, const int* o_rows, long long bias_us,
+                     const __half* btab_ext, long long btab_us, cudaStream_t st) {
   using namespace attng;
   if (b_row != BQ || b_col != BQ || (dh != 64 && dh != 80) || S < 1 || bias_w > 64 || !(tau > 0.f)) return 1;
   Params p{};
@@ -682,13 +688,18 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
   p.off_bar = take(256, 8);
   const size_t smem = 1024 + (size_t)off;
   if (smem > 227 * 1024) return 1;
-  // fp16 bias operand rows [heads, S, 128] (scratch, grow-only per device)
-  {
+  // fp16 bias operand rows [heads, S, 128] (scratch, grow-only per device); per-unit fp32
+  // tables (contiguous: bias_us == heads * S * w) -> [units, heads, S, 128]; or the caller's
+  if (bias_us && !btab_ext && bias_us != (long long)heads * S * bias_w) return 1;
+  if (btab_ext) {
+    p.btab = btab_ext;
+    p.btab_us = btab_us;
+  } else {
     static __half* buf[64] = {nullptr};
     static size_t cap[64] = {0};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return ZS_ERR_DEVICE;
-    const size_t need = (size_t)heads * S * 128;
+    const size_t need = (size_t)heads * S * 128 * (bias_us ? units : 1);
     if (cap[dev] < need) {
       if (buf[dev]) cudaFree(buf[dev]);
       buf[dev] = nullptr;
@@ -697,9 +708,10 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
       cap[dev] = need;
     }
     const long long n = (long long)need;
-    glob_bias_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(bh, bw, heads * S, bias_w, 1.0f / tau,
+    glob_bias_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(bh, bw, n / 128, bias_w, 1.0f / tau,
                                                                         buf[dev]);
     p.btab = buf[dev];
+    p.btab_us = bias_us ? (long long)heads * S * 128 : 0;
   }
   CUtensorMap m[6];
   const uint64_t ncol = (uint64_t)heads * dh;

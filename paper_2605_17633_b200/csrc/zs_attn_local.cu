@@ -34,6 +34,7 @@ struct Params {
   long long ldo, o_unit_stride;
   const int* o_rows;  // optional: output row of (unit, query row), -1 = not written
   const float* bh;
+  long long bias_us;  // floats between the bh / bw tables of consecutive units (0: shared)
   const float* bw;
   const int* q_sp;
   const int* k_sp;
@@ -268,8 +269,9 @@ __global__ void __launch_bounds__(attnl::kThreads, 1)
     auto stage_bias = [&](int it) {
       const int u = it / P.heads, h = it % P.heads;
       const int sp = P.q_sp[(long long)u * P.sq + min(row, P.sq - 1)];
-      const float* sh = P.bh + ((long long)h * P.sq + sp) * P.bias_w;
-      const float* sw = P.bw + ((long long)h * P.sq + sp) * P.bias_w;
+      const long long bo = (long long)u * P.bias_us + ((long long)h * P.sq + sp) * P.bias_w;
+      const float* sh = P.bh + bo;
+      const float* sw = P.bw + bo;
       for (int j = 0; j < P.bias_w; ++j) {
         cp_async4(my_bias + j, sh + j);
         cp_async4(my_bias + W1 + j, sw + j);
@@ -475,8 +477,10 @@ using namespace zs;
 int launch_attn_local(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                       long long qus, long long kvus, int units, int heads, int sq, int sk, int dh, const float* bh,
                       const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col,
-                      int prefix, float tau, void* out, long long ldo, long long ous, const int* o_rows, cudaStream_t st) {
+                      int prefix, float tau, void* out, long long ldo, long long ous, const int* o_rows,
+                      long long bias_us, cudaStream_t st) {
   attnl::Params p;
+  p.bias_us = bias_us;
   p.units = units;
   p.heads = heads;
   p.sq = sq;

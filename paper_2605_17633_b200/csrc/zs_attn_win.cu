@@ -46,6 +46,7 @@ struct Params {
   long long ldo, o_unit_stride;
   const int* o_rows;  // optional: output row of (unit, query row), -1 = not written
   const __half* btab;  // [heads, S, 32] fp16: bh/tau (cols 0..15), bw/tau (16..31), zero padded
+  long long btab_us;   // halves between the tables of consecutive units (0: one table for all)
   const __half* kb1;   // [S, 32] fp16 one-hot rows of every spatial key: e_{s/w} | e_{s%w}
   const int* q_sp;
   const int* k_sp;
@@ -185,16 +186,17 @@ __device__ __forceinline__ void tmem_zero(uint32_t pa, bool w32) {
 
 // [heads*S, 32] fp16 bias operand rows (bh/tau, 0-pad to 16, bw/tau, 0-pad to 16), followed by
 // the [S, 32] one-hot key rows (e_{s/w}, e_{s%w})
-__global__ void win_bias_prep_kernel(const float* __restrict__ bh, const float* __restrict__ bw, int rows, int S,
-                                     int w, float inv_tau, __half* __restrict__ out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r = i >> 5, c = i & 31, j = c & 15;
+__global__ void win_bias_prep_kernel(const float* __restrict__ bh, const float* __restrict__ bw, long long rows,
+                                     int S, int w, float inv_tau, __half* __restrict__ out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long r = i >> 5;
+  const int c = (int)(i & 31), j = c & 15;
   if (r < rows) {
     float v = 0.f;
     if (j < w) v = (c < 16 ? bh : bw)[(long long)r * w + j] * inv_tau;
     out[i] = __float2half_rn(v);
   } else if (r < rows + S) {
-    const int sp = r - rows;
+    const int sp = (int)(r - rows);
     out[i] = __float2half_rn(j == (c < 16 ? sp / w : sp % w) ? 1.f : 0.f);
   }
 }
@@ -410,7 +412,7 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
           const int j = lane + 32 * i;
           idx[i] = j < P.S ? __ldg(isrc + j) : -1;
         }
-        const __half* tab = is_q ? P.btab + (long long)h * P.S * 32 : P.kb1;
+        const __half* tab = is_q ? P.btab + (long long)u * P.btab_us + (long long)h * P.S * 32 : P.kb1;
         mbar_wait_sleep(bk_empty, (k & 1) ^ 1);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -615,7 +617,8 @@ static __half* win_btab(size_t elems) {
 int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                     long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
                     const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
-                    float tau, void* out, long long ldo, long long ous, const int* o_rows, cudaStream_t st) {
+                    float tau, void* out, long long ldo, long long ous, const int* o_rows, long long bias_us,
+                    const __half* btab_ext, long long btab_us, cudaStream_t st) {
   using namespace attnw;
   if (S <= 0 || S > 256 || (b_row % 32) || (b_col % 32) || (dh != 64 && dh != 80)) return 1;
   if (bias_w > 16 || bias_w * bias_w != S || !(tau > 0.f)) return 1;
@@ -740,15 +743,20 @@ int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, 
   const int row_b = dh * 2;  // TMA boxes count their OOB (zero-filled) rows too
   p.tx_qk = (p.nt > 1 ? 128 + rb + 128 + rb : 128 + 128) * row_b;
   p.tx_v = (p.nt > 1 ? 128 + rb : 128) * row_b;
-  // fp16 bias operand rows [heads, S, 32] (bh, bw scaled by 1/tau)
-  __half* btab = win_btab((size_t)(heads + 1) * S * 32);
+  // fp16 bias operand rows (bh, bw scaled by 1/tau): [heads, S, 32], or [units, heads, S, 32]
+  // for per-unit fp32 tables (contiguous, bias_us == heads * S * w), or the caller's btab_ext;
+  // followed by the [S, 32] one-hot key rows
+  if (bias_us && !btab_ext && bias_us != (long long)heads * S * bias_w) return 1;
+  const long long trows = btab_ext ? 0 : (long long)heads * S * (bias_us ? units : 1);
+  __half* btab = win_btab((size_t)(trows + S) * 32);
   if (!btab) return ZS_ERR_DEVICE;
   {
-    const int n = (heads + 1) * S * 32;
-    win_bias_prep_kernel<<<(n + 255) / 256, 256, 0, st>>>(bh, bw, heads * S, S, bias_w, 1.0f / tau, btab);
+    const long long n = (trows + S) * 32;
+    win_bias_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(bh, bw, trows, S, bias_w, 1.0f / tau, btab);
   }
-  p.btab = btab;
-  p.kb1 = btab + (size_t)heads * S * 32;
+  p.btab = btab_ext ? btab_ext : btab;
+  p.btab_us = btab_ext ? btab_us : (bias_us ? (long long)heads * S * 32 : 0);
+  p.kb1 = btab + trows * 32;
   CUtensorMap m[12];
   const uint64_t ncol = (uint64_t)heads * dh;
   int rc = 0;

@@ -237,8 +237,8 @@ def stripe_attn(
     sq: int,
     sk: int,
     dh: int,
-    bh: torch.Tensor,
-    bw: torch.Tensor,
+    bh: torch.Tensor | None,
+    bw: torch.Tensor | None,
     q_sp: torch.Tensor,
     k_sp: torch.Tensor,
     b_row: int,
@@ -249,25 +249,59 @@ def stripe_attn(
     q_unit_stride: int | None = None,
     kv_unit_stride: int | None = None,
     o_rows: torch.Tensor | None = None,
+    rel_pos: tuple[torch.Tensor, torch.Tensor] | None = None,
 ) -> torch.Tensor:
     """Block-sparse stripe attention.  q/k/v are row-major views ``[units*S, ld]``
     whose head ``h`` lives at columns ``h*dh``; ``out`` is ``[units*sq, heads*dh]``, or, with
     ``o_rows`` (int32 ``[units*sq]``), query row r of unit u goes to ``out[o_rows[u*sq + r]]``
-    and is skipped where ``o_rows < 0``."""
+    and is skipped where ``o_rows < 0``.
+
+    Bias: ``bh``/``bw`` fp32 ``[heads, S, w]`` (one table pair, the reference's BiasTables) or
+    ``[units, heads, S, w]`` (one pair per unit); or ``rel_pos=(rel_pos_h, rel_pos_w)`` (fp32
+    ``[2w-1, dh]``, bh = bw = None): SAM's q-dependent decomposed bias, computed on the fly."""
     for t, n in ((q, "q"), (k, "k"), (v, "v")):
         _need(t, torch.bfloat16, n)
         if t.stride(-1) != 1:
             raise ValueError(f"{n} must be column-contiguous")
-    _need(bh, torch.float32, "bh")
-    _need(bw, torch.float32, "bw")
     _need(q_sp, torch.int32, "q_sp")
     _need(k_sp, torch.int32, "k_sp")
-    bias_w = bh.shape[-1]
     if out is None:
         out = torch.empty((units * sq, heads * dh), device=q.device, dtype=torch.bfloat16)
     ldq, ldk, ldv = q.stride(0), k.stride(0), v.stride(0)
     qus = q_unit_stride if q_unit_stride is not None else sq * ldq
     kvus = kv_unit_stride if kv_unit_stride is not None else sk * ldk
+    if o_rows is not None:
+        _need(o_rows, torch.int32, "o_rows")
+        if o_rows.numel() < units * sq:
+            raise ValueError("o_rows must hold units*sq entries")
+    if rel_pos is not None:
+        rh, rw = (t.contiguous() for t in rel_pos)
+        _need(rh, torch.float32, "rel_pos_h")
+        _need(rw, torch.float32, "rel_pos_w")
+        bias_w = (rh.shape[0] + 1) // 2
+        if sq != sk or rh.shape != (2 * bias_w - 1, dh) or rw.shape != rh.shape:
+            raise ValueError("rel_pos tables must be [2w-1, dh] with sq == sk == w*w")
+        ws = relpos_workspace(units, heads, sq, dh, bias_w, q.device)
+        _lib.call(
+            "zs_stripe_attn_fwd_relpos", _ptr(q), _ptr(k), _ptr(v), ldq, ldk, ldv, qus, kvus, units, heads, sq, dh,
+            _ptr(rh), _ptr(rw), bias_w, _ptr(q_sp), _ptr(k_sp), b_row, b_col, prefix, float(tau), _ptr(out),
+            out.stride(0), sq * out.stride(0), _ptr(o_rows) if o_rows is not None else None, _ptr(ws), ws.numel(),
+            _stream(),
+        )
+        return out
+    _need(bh, torch.float32, "bh")
+    _need(bw, torch.float32, "bw")
+    bias_w = bh.shape[-1]
+    if bh.dim() == 4:
+        if bh.shape[0] != units or bw.shape != bh.shape:
+            raise ValueError("per-unit bias tables must be [units, heads, S, w]")
+        bh, bw = bh.contiguous(), bw.contiguous()
+        _lib.call(
+            "zs_stripe_attn_fwd_unit_bias", _ptr(q), _ptr(k), _ptr(v), ldq, ldk, ldv, qus, kvus, units, heads, sq, sk,
+            dh, _ptr(bh), _ptr(bw), bh[0].numel(), bias_w, _ptr(q_sp), _ptr(k_sp), b_row, b_col, prefix, float(tau),
+            _ptr(out), out.stride(0), sq * out.stride(0), _ptr(o_rows) if o_rows is not None else None, _stream(),
+        )
+        return out
     if o_rows is None:
         _lib.call(
             "zs_stripe_attn_fwd", _ptr(q), _ptr(k), _ptr(v), ldq, ldk, ldv, qus, kvus, units, heads, sq, sk, dh,
@@ -275,15 +309,47 @@ def stripe_attn(
             float(tau), _ptr(out), out.stride(0), sq * out.stride(0), _stream(),
         )
     else:
-        _need(o_rows, torch.int32, "o_rows")
-        if o_rows.numel() < units * sq:
-            raise ValueError("o_rows must hold units*sq entries")
         _lib.call(
             "zs_stripe_attn_fwd_rows", _ptr(q), _ptr(k), _ptr(v), ldq, ldk, ldv, qus, kvus, units, heads, sq, sk, dh,
             _ptr(bh.contiguous()), _ptr(bw.contiguous()), bias_w, _ptr(q_sp), _ptr(k_sp), b_row, b_col, prefix,
             float(tau), _ptr(out), out.stride(0), sq * out.stride(0), _ptr(o_rows), _stream(),
         )
     return out
+
+
+_RELPOS_WS: dict = {}
+
+
+def relpos_workspace(units: int, heads: int, S: int, dh: int, bias_w: int, device) -> torch.Tensor:
+    """Grow-only per-device workspace of the SAM rel-pos path (zs_relpos_ws_bytes)."""
+    need = int(_lib.load().zs_relpos_ws_bytes(units, heads, S, dh, bias_w))
+    if need <= 0:
+        raise ValueError(f"rel-pos mode unsupported for S={S}, dh={dh}, w={bias_w}")
+    key = torch.device(device)
+    ws = _RELPOS_WS.get(key)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(need, dtype=torch.uint8, device=key)
+        _RELPOS_WS[key] = ws
+    return ws
+
+
+def relpos_bias(q: torch.Tensor, *, units: int, heads: int, S: int, dh: int, rel_pos_h: torch.Tensor,
+                rel_pos_w: torch.Tensor, q_sp: torch.Tensor, q_unit_stride: int | None = None):
+    """SAM's decomposed rel-pos terms as per-unit BiasTables: (bh, bw) fp32 [units, heads, S, w],
+    bh[u, h, s, ky] = q_h(row of s) . rel_pos_h[s // w - ky + w - 1] (unscaled q; s = q_sp[u, row])."""
+    _need(q, torch.bfloat16, "q")
+    _need(q_sp, torch.int32, "q_sp")
+    rh, rw = rel_pos_h.contiguous(), rel_pos_w.contiguous()
+    _need(rh, torch.float32, "rel_pos_h")
+    _need(rw, torch.float32, "rel_pos_w")
+    w = (rh.shape[0] + 1) // 2
+    bh = torch.empty((units, heads, S, w), device=q.device, dtype=torch.float32)
+    bw = torch.empty_like(bh)
+    ws = relpos_workspace(units, heads, S, dh, w, q.device)
+    qus = q_unit_stride if q_unit_stride is not None else S * q.stride(0)
+    _lib.call("zs_relpos_bias", _ptr(q), q.stride(0), qus, units, heads, S, dh, w, _ptr(rh), _ptr(rw), _ptr(q_sp),
+              _ptr(bh), _ptr(bw), _ptr(ws), ws.numel(), _stream())
+    return bh, bw
 
 
 def invert_rows(rows: torch.Tensor, map_len: int, n_dev: torch.Tensor | None = None,

@@ -15,7 +15,7 @@ from paper_2605_17633_b200 import _lib  # noqa: E402
 
 
 def header_symbols():
-    return sorted(set(re.findall(r"^ZS_API\s+(?:const\s+char\s*\*|int)\s+(zs_\w+)\(", HEADER.read_text(), re.M)))
+    return sorted(set(re.findall(r"^ZS_API\s+(?:const\s+char\s*\*|int|size_t)\s+(zs_\w+)\(", HEADER.read_text(), re.M)))
 
 
 @pytest.fixture(scope="module")
@@ -41,7 +41,7 @@ def test_every_declared_symbol_is_exported(lib):
 def test_binding_arity_matches_header(lib):
     text = HEADER.read_text()
     for name, args in _lib.SIGNATURES.items():
-        m = re.search(rf"ZS_API\s+int\s+{name}\(([^;]*)\);", text, re.S)
+        m = re.search(rf"ZS_API\s+(?:int|size_t)\s+{name}\(([^;]*)\);", text, re.S)
         assert m, name
         params = [p for p in m.group(1).split(",") if p.strip() and p.strip() != "void"]
         assert len(params) == len(args), (name, len(params), len(args))

@@ -219,12 +219,12 @@ def test_rank_ties_and_nan_follow_numpy_lexsort():
 
 
 # ---------------------------------------------------------------- attention
-def _attn_case(units, heads, S, dh, w, tile, r, seed=0):
+def _attn_case(units, heads, S, dh, w, tile, r, seed=0, bscale=0.5):
     g = torch.Generator().manual_seed(seed)
     C = heads * dh
     qkv = torch.randn(units * S, 3 * C, generator=g).bfloat16().to(DEV)
-    bh = (0.5 * torch.randn(heads, S, w, generator=g)).to(DEV)
-    bw = (0.5 * torch.randn(heads, S, w, generator=g)).to(DEV)
+    bh = (bscale * torch.randn(heads, S, w, generator=g)).to(DEV)
+    bw = (bscale * torch.randn(heads, S, w, generator=g)).to(DEV)
     sp = torch.stack([torch.randperm(S, generator=g) for _ in range(units)]).int().to(DEV)
     T = -(-S // tile)
     out = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], units=units, heads=heads, sq=S, sk=S, dh=dh,
@@ -280,6 +280,15 @@ def test_attention_window_kernels_agree(r, monkeypatch):
 @pytest.mark.parametrize("r", [0.2, 0.4, 1.0])
 def test_attention_global(dh, r):
     assert _attn_case(2, 2, 4096, dh, 64, 128, r) < 1e-2
+
+
+@pytest.mark.parametrize("S,w,tile", [(4096, 64, 128), (196, 14, 32)])
+def test_attention_large_bias(S, w, tile):
+    """Bias spread far beyond the lazy-rescale threshold (ln 256): rows move their reference max
+    on many chunks, so the O rescale runs mid-item, for some rows of a warp only."""
+    units = 2 if S > 256 else 8
+    assert _attn_case(units, 2, S, 80, w, tile, 0.4, seed=5, bscale=6.0) < 1e-2
+    assert _attn_case(units, 2, S, 64, w, tile, 1.0, seed=6, bscale=6.0) < 1e-2
 
 
 @pytest.mark.parametrize("dh", [64, 80])
