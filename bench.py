@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no side legs)")
+    ap.add_argument("--rel-pos", default="static", choices=["static", "sam"],
+                    help="static: the reference's BiasTables (the headline config); sam: SAM's q-dependent "
+                         "decomposed rel-pos (rel_pos_h / rel_pos_w tables, bias computed per query)")
     return ap.parse_args()
 
 
@@ -193,7 +196,7 @@ def main():
         args.warmup = 3
 
     cfg = sam_config(args.model, args.density)
-    params = random_params(cfg, dev, seed=0)
+    params = random_params(cfg, dev, seed=0, rel_pos=args.rel_pos == "sam")
     frame = random_frame(cfg, dev, seed=1)
     enc = SparseSAMImageEncoder(cfg, params, frame, dev)
     a, b = shard_bounds(args.batch, world, rank)
@@ -357,7 +360,7 @@ def main():
             "config": {"workload": f"full SAM {args.model} image encoder (patch embed, 32 blocks, neck), "
                                    f"density {args.density}, 1024x1024 synthetic images, random-init weights",
                        "model": f"sam_{args.model}", "global_batch": args.batch, "per_gpu_batch": nloc,
-                       "seq_len": 4096, "parallelism": f"image-sharded dp{world}",
+                       "seq_len": 4096, "parallelism": f"image-sharded dp{world}", "rel_pos": args.rel_pos,
                        "l2": "inputs larger than L2 (batch of images > 126 MB); no explicit flush"},
             "e2e": e2e, "dense_baseline": dense, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": launches, "kernels": kernels,

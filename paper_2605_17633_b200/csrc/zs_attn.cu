@@ -704,7 +704,7 @@ namespace zs {
 size_t relpos_r_bytes(int dh, int w);
 int launch_relpos(const void* q, long long ldq, long long qus, int units, int heads, int S, int dh, int w,
                   const float* rel_h, const float* rel_w, const int* q_sp, float tau, int mode, __half* btab,
-                  long long btab_us, float* bh, float* bw, void* ws, cudaStream_t st);
+                  long long btab_us, int w16, float* bh, float* bw, void* ws, cudaStream_t st);
 }  // namespace zs
 
 template <int DH, bool FAST>
@@ -888,7 +888,7 @@ extern "C" int zs_stripe_attn_fwd_unit_bias(const void* q, const void* k, const 
 
 // ---------------------------------------------------------------- SAM relative-position mode
 static size_t relpos_tables_bytes(int units, int heads, int S, int bias_w) {
-  const size_t w16 = 2 * (size_t)((bias_w + 15) & ~15);
+  const size_t w16 = S <= 256 ? 32 : 128;
   const size_t op = (size_t)units * heads * S * w16 * 2;           // fp16 operand rows
   const size_t f32 = 2 * (size_t)units * heads * S * bias_w * 4;   // fp32 bh, bw (fallback kernels)
   return ((op > f32 ? op : f32) + 255) & ~(size_t)255;
@@ -910,7 +910,7 @@ extern "C" int zs_relpos_bias(const void* q, long long ldq, long long q_unit_str
   if (((ldq | q_unit_stride) & 7) || (reinterpret_cast<uintptr_t>(q) & 15) || (reinterpret_cast<uintptr_t>(ws) & 255))
     return ZS_ERR_ALIGN;
   const int rc = launch_relpos(q, ldq, q_unit_stride, units, heads, S, dh, bias_w, rel_pos_h, rel_pos_w, q_sp, 1.0f, 1,
-                               nullptr, 0, bh, bw, ws, reinterpret_cast<cudaStream_t>(stream));
+                               nullptr, 0, 0, bh, bw, ws, reinterpret_cast<cudaStream_t>(stream));
   return rc == 1 ? ZS_ERR_SHAPE : rc;
 }
 
@@ -928,14 +928,16 @@ extern "C" int zs_stripe_attn_fwd_relpos(const void* q, const void* k, const voi
   if (reinterpret_cast<uintptr_t>(ws) & 255) return ZS_ERR_ALIGN;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   uint8_t* tables = reinterpret_cast<uint8_t*>(ws) + relpos_r_bytes(dh, bias_w);
-  // fast kernels: fp16 operand rows straight from the relpos GEMM epilogue
-  const bool fast_shape = (S <= 256) ? (b_row % 32 == 0 && b_col % 32 == 0) : (b_row == 128 && b_col == 128);
+  // fast kernels: fp16 operand rows straight from the relpos GEMM epilogue, in the row width
+  // the consuming kernel reads (window kernel: 16 + 16 halves, w <= 16; global: 64 + 64)
+  const bool fast_shape = (S <= 256) ? (b_row % 32 == 0 && b_col % 32 == 0 && bias_w <= 16)
+                                     : (b_row == 128 && b_col == 128);
   if (fast_shape) {
-    const long long w16 = 2 * ((bias_w + 15) & ~15);
+    const int w16 = S <= 256 ? 32 : 128;
     const long long us = (long long)heads * S * w16;
     __half* btab = reinterpret_cast<__half*>(tables);
     int rc = launch_relpos(q, ldq, q_unit_stride, units, heads, S, dh, bias_w, rel_pos_h, rel_pos_w, q_sp, tau, 0,
-                           btab, us, nullptr, nullptr, ws, st);
+                           btab, us, w16, nullptr, nullptr, ws, st);
     if (rc < 0) return rc;
     if (rc == 0) {
       rc = attn_dispatch(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, S, S, dh, nullptr,

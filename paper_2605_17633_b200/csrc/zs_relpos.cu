@@ -230,8 +230,9 @@ __global__ void __launch_bounds__(relpos::kThreads, 1)
   if (warp == 2) tmem_dealloc(tmem, 2 * NB < 32 ? 32 : 2 * NB);
 }
 
-// Host launcher (internal).  mode 0 -> fp16 operand rows into btab (unit stride btab_us
-// halves); mode 1 -> fp32 bh / bw [units, heads, S, w].  ws: >= relpos_ws_r_bytes() bytes for
+// Host launcher (internal).  mode 0 -> fp16 operand rows of w16 halves (bh/tau at [0, w),
+// bw/tau at [w16/2, w16/2 + w)) into btab (unit stride btab_us halves); mode 1 -> fp32 bh / bw
+// [units, heads, S, w].  ws: >= relpos_ws_r_bytes() bytes for
 // the bf16 R table.  Returns 1 when the shape is outside the kernel (w > 64, dh not 64/80).
 size_t relpos_r_bytes(int dh, int w) {
   const int nb = 2 * (2 * w - 1) <= 64 ? 64 : (2 * (2 * w - 1) <= 128 ? 128 : 256);
@@ -240,9 +241,10 @@ size_t relpos_r_bytes(int dh, int w) {
 
 int launch_relpos(const void* q, long long ldq, long long qus, int units, int heads, int S, int dh, int w,
                   const float* rel_h, const float* rel_w, const int* q_sp, float tau, int mode, __half* btab,
-                  long long btab_us, float* bh, float* bw, void* ws, cudaStream_t st) {
+                  long long btab_us, int w16, float* bh, float* bw, void* ws, cudaStream_t st) {
   using namespace relpos;
   if ((dh != 64 && dh != 80) || w < 1 || w > 64 || w * w != S || !(tau > 0.f)) return 1;
+  if (mode == 0 && (w16 % 16 || w16 < 2 * ((w + 15) & ~15))) return 1;
   const int nr = 2 * w - 1;
   const int nb = 2 * nr <= 64 ? 64 : (2 * nr <= 128 ? 128 : 256);
   Params p{};
@@ -260,7 +262,7 @@ int launch_relpos(const void* q, long long ldq, long long qus, int units, int he
   p.inv_tau = 1.0f / tau;
   p.btab = btab;
   p.btab_us = btab_us;
-  p.w16 = 2 * ((w + 15) & ~15);
+  p.w16 = w16;
   p.bh = bh;
   p.bw = bw;
   int off = 0;

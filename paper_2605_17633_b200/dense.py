@@ -28,12 +28,26 @@ def dense_bias(bh: torch.Tensor, bw: torch.Tensor) -> torch.Tensor:
     return (bh[:, :, k // w] + bw[:, :, k % w]).to(torch.bfloat16).contiguous()
 
 
+def sam_rel_pos_bias(q: torch.Tensor, rel_h: torch.Tensor, rel_w: torch.Tensor) -> torch.Tensor:
+    """SAM add_decomposed_rel_pos as an additive mask: q [N, H, S, dh] (unscaled, spatial row-major
+    order, S = w * w), rel_h / rel_w [2w - 1, dh] -> [N, H, S, S] bias in q's dtype."""
+    N, H, S, dh = q.shape
+    w = (rel_h.shape[0] + 1) // 2
+    idx = torch.arange(w, device=q.device)
+    rel = idx[:, None] - idx[None, :] + w - 1  # [qy, ky] -> table row
+    Rh, Rw = rel_h.to(q.dtype)[rel], rel_w.to(q.dtype)[rel]  # [w, w, dh]
+    r_q = q.reshape(N, H, w, w, dh)
+    bh = torch.einsum("nhyxc,ykc->nhyxk", r_q, Rh)  # [N, H, qy, qx, ky]
+    bw = torch.einsum("nhyxc,xkc->nhyxk", r_q, Rw)  # [N, H, qy, qx, kx]
+    return (bh[..., :, None] + bw[..., None, :]).reshape(N, H, S, S)
+
+
 class DenseSAMEncoder:
     def __init__(self, cfg: EncoderConfig, params: list[BlockParams], frame: FrameParams | None = None):
         self.cfg = cfg
         self.params = params
         self.frame = frame
-        self.bias = [dense_bias(p.bh, p.bw) for p in params]
+        self.bias = [dense_bias(p.bh, p.bw) if p.rel_pos_h is None else None for p in params]
 
     def _attn(self, x, p: BlockParams, bias):
         # x [N, S, C] bf16
@@ -42,7 +56,11 @@ class DenseSAMEncoder:
         dh = C // H
         h = F.layer_norm(x.float(), (C,), p.ln1_g, p.ln1_b, 1e-6).to(torch.bfloat16)
         qkv = F.linear(h, p.qkv_w, p.qkv_b.to(torch.bfloat16)).view(N, S, 3, H, dh).permute(2, 0, 3, 1, 4)
-        o = F.scaled_dot_product_attention(qkv[0], qkv[1], qkv[2], attn_mask=bias[None].expand(N, -1, -1, -1))
+        if bias is None:  # SAM rel-pos mode: q-dependent bias
+            mask = sam_rel_pos_bias(qkv[0], p.rel_pos_h, p.rel_pos_w)
+        else:
+            mask = bias[None].expand(N, -1, -1, -1)
+        o = F.scaled_dot_product_attention(qkv[0], qkv[1], qkv[2], attn_mask=mask)
         o = o.transpose(1, 2).reshape(N, S, C)
         return F.linear(o, p.proj_w, p.proj_b.to(torch.bfloat16))
 

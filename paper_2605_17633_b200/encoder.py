@@ -199,8 +199,10 @@ class StripeSortEncoder:
         sig = od.sigma_loc if local else od.sigma_glob
         xs = x[:R]
         tr = self.tracer
-        w = blk.bh.shape[-1]
+        w = blk.side
         E = attention_elements(S, tile, prefix)
+        bias = (dict(bh=None, bw=None, rel_pos=(blk.rel_pos_h, blk.rel_pos_w)) if blk.rel_pos_h is not None
+                else dict(bh=blk.bh, bw=blk.bw))
         if nonpad is not None:
             # non-pad rows only (compacted), pad K/V rows = the constant row of LN(0) = beta
             npr, nn, mx = nonpad["rows"], nonpad["n"], nonpad["max"]
@@ -212,8 +214,8 @@ class StripeSortEncoder:
             with tr.span(f"attn_{blk.kind}", flops=4.0 * dh * E * U * H,
                          bytes=U * H * 4 * S * dh * 2 + H * 2 * S * w * 4):
                 o = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], units=U, heads=H, sq=S, sk=S, dh=dh,
-                                  bh=blk.bh, bw=blk.bw, q_sp=sig, k_sp=sig, b_row=tile, b_col=tile, prefix=prefix,
-                                  tau=1.0 / math.sqrt(dh), out=ws["o"][:R], o_rows=nonpad["omap"])
+                                  q_sp=sig, k_sp=sig, b_row=tile, b_col=tile, prefix=prefix,
+                                  tau=1.0 / math.sqrt(dh), out=ws["o"][:R], o_rows=nonpad["omap"], **bias)
             with tr.span("gemm_proj", flops=(nn, 2.0 * C * C)):
                 K.gemm(o[:mx], blk.proj_w, blk.proj_b, epi=K.EPI_F32_RESID, out=xs, res=xs, row_map=npr, m_dev=nn)
         else:
@@ -224,8 +226,8 @@ class StripeSortEncoder:
             with tr.span(f"attn_{blk.kind}", flops=4.0 * dh * E * U * H,
                          bytes=U * H * 4 * S * dh * 2 + H * 2 * S * w * 4):
                 o = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], units=U, heads=H, sq=S, sk=S, dh=dh,
-                                  bh=blk.bh, bw=blk.bw, q_sp=sig, k_sp=sig, b_row=tile, b_col=tile, prefix=prefix,
-                                  tau=1.0 / math.sqrt(dh), out=ws["o"][:R])
+                                  q_sp=sig, k_sp=sig, b_row=tile, b_col=tile, prefix=prefix,
+                                  tau=1.0 / math.sqrt(dh), out=ws["o"][:R], **bias)
             with tr.span("gemm_proj", flops=2.0 * R * C * C, bytes=R * C * 2 + C * C * 2 + R * C * 8):
                 K.gemm(o, blk.proj_w, blk.proj_b, epi=K.EPI_F32_RESID, out=xs, res=xs,
                        zero_rows=od.maps["l_is_pad"] if local else None)

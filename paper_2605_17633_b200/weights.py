@@ -27,14 +27,23 @@ class BlockParams:
     qkv_b: torch.Tensor  # [3C]
     proj_w: torch.Tensor  # [C, C] bf16
     proj_b: torch.Tensor
-    bh: torch.Tensor  # [H, S_attn, w] fp32
-    bw: torch.Tensor
+    bh: torch.Tensor | None  # [H, S_attn, w] fp32 static tables (reference BiasTables), or None
+    bw: torch.Tensor | None
     ln2_g: torch.Tensor
     ln2_b: torch.Tensor
     w1: torch.Tensor  # [4C, C] bf16
     b1: torch.Tensor
     w2: torch.Tensor  # [C, 4C] bf16
     b2: torch.Tensor
+    # SAM relative-position mode: fp32 [2w - 1, dh] tables shared by the
+    # heads; the bias is then q-dependent (SAM add_decomposed_rel_pos) and bh / bw are None
+    rel_pos_h: torch.Tensor | None = None
+    rel_pos_w: torch.Tensor | None = None
+
+    @property
+    def side(self) -> int:
+        """Side w of the attention grid (S = w * w)."""
+        return int(self.bh.shape[-1]) if self.bh is not None else (int(self.rel_pos_h.shape[0]) + 1) // 2
 
 
 def _f32(a, dev):
@@ -88,9 +97,11 @@ def params_from_reference(blocks, cfg: EncoderConfig, device) -> list[BlockParam
     return [block_from_reference(b, k, device) for b, k in zip(blocks, cfg.layout)]
 
 
-def random_params(cfg: EncoderConfig, device, seed: int = 0) -> list[BlockParams]:
+def random_params(cfg: EncoderConfig, device, seed: int = 0, rel_pos: bool = False,
+                  rel_pos_std: float = 0.05) -> list[BlockParams]:
     """Seeded random weights with the reference's init statistics (encoder.py:192-229),
-    drawn on the device (a ViT-H has 0.63 B parameters)."""
+    drawn on the device (a ViT-H has 0.63 B parameters).  ``rel_pos``: SAM relative-position
+    tables N(0, rel_pos_std) [2w - 1, dh] per block instead of the static bias tables."""
     g = torch.Generator(device=device).manual_seed(seed)
     d, hid, H = cfg.d, 4 * cfg.d, cfg.heads
     f32 = dict(device=device, dtype=torch.float32)
@@ -110,14 +121,16 @@ def random_params(cfg: EncoderConfig, device, seed: int = 0) -> list[BlockParams
                 qkv_b=torch.zeros(3 * d, **f32),
                 proj_w=rn((d, d), 1.0 / math.sqrt(d)).bfloat16(),
                 proj_b=torch.zeros(d, **f32),
-                bh=rn((H, s_attn, side), 0.5),
-                bw=rn((H, s_attn, side), 0.5),
+                bh=None if rel_pos else rn((H, s_attn, side), 0.5),
+                bw=None if rel_pos else rn((H, s_attn, side), 0.5),
                 ln2_g=torch.ones(d, **f32),
                 ln2_b=torch.zeros(d, **f32),
                 w1=rn((hid, d), 1.0 / math.sqrt(d)).bfloat16(),
                 b1=torch.zeros(hid, **f32),
                 w2=rn((d, hid), 1.0 / math.sqrt(hid)).bfloat16(),
                 b2=torch.zeros(d, **f32),
+                rel_pos_h=rn((2 * side - 1, cfg.head_dim), rel_pos_std) if rel_pos else None,
+                rel_pos_w=rn((2 * side - 1, cfg.head_dim), rel_pos_std) if rel_pos else None,
             )
         )
     return out

@@ -109,7 +109,8 @@ def test_unit_bias_attention_vs_oracle(S, w, tile, r):
 
 
 @pytest.mark.parametrize("S,w,tile,r,dh", [(196, 14, 32, 0.4, 80), (196, 14, 32, 0.2, 64), (196, 14, 32, 1.0, 80),
-                                           (4096, 64, 128, 0.4, 80), (4096, 64, 128, 0.2, 64)])
+                                           (4096, 64, 128, 0.4, 80), (4096, 64, 128, 0.2, 64), (1024, 32, 128, 0.4, 80),
+                                           (144, 12, 32, 0.5, 80), (784, 28, 128, 0.6, 64)])
 def test_relpos_attention_matches_twin_tables(S, w, tile, r, dh):
     """Fused SAM mode (tables straight into the kernels' fp16 operand rows; r = 1 windows take
     the fp32-table fallback) == the same attention fed the fp32 twin's per-unit tables, and
@@ -143,3 +144,51 @@ def test_relpos_argument_errors():
         K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], units=2, heads=2, sq=196, sk=196, dh=80,
                       bh=torch.zeros(3, 2, 196, 14, device=DEV), bw=torch.zeros(3, 2, 196, 14, device=DEV), q_sp=sp,
                       k_sp=sp, b_row=32, b_col=32, prefix=2, tau=0.1)
+
+
+def _twin_blocks(x, params, cfg):
+    """fp32 torch twin of SAM blocks with decomposed rel-pos (windows without pads), r = keep = 1."""
+    import torch.nn.functional as F
+
+    from paper_2605_17633_b200.dense import sam_rel_pos_bias
+
+    B, Hh, Ww, C = x.shape
+    H, win = cfg.heads, cfg.window
+    dh = C // H
+    for p in params:
+        if p.kind == "local":
+            t = x.view(B, Hh // win, win, Ww // win, win, C).permute(0, 1, 3, 2, 4, 5).reshape(-1, win * win, C)
+        else:
+            t = x.reshape(B, Hh * Ww, C)
+        N, S, _ = t.shape
+        h = F.layer_norm(t, (C,), p.ln1_g, p.ln1_b, 1e-6)
+        qkv = (h @ p.qkv_w.float().T + p.qkv_b).view(N, S, 3, H, dh).permute(2, 0, 3, 1, 4)
+        q, k, v = qkv[0], qkv[1], qkv[2]
+        att = (q * dh ** -0.5) @ k.transpose(-1, -2) + sam_rel_pos_bias(q, p.rel_pos_h, p.rel_pos_w)
+        o = (att.softmax(-1) @ v).transpose(1, 2).reshape(N, S, C)
+        t = t + o @ p.proj_w.float().T + p.proj_b
+        hh = F.layer_norm(t, (C,), p.ln2_g, p.ln2_b, 1e-6)
+        t = t + F.gelu(hh @ p.w1.float().T + p.b1) @ p.w2.float().T + p.b2
+        if p.kind == "local":
+            x = t.view(B, Hh // win, Ww // win, win, win, C).permute(0, 1, 3, 2, 4, 5).reshape(B, Hh, Ww, C)
+        else:
+            x = t.view(B, Hh, Ww, C)
+    return x
+
+
+def test_encoder_rel_pos_mode_vs_fp32_twin():
+    """Whole local + global blocks in SAM rel-pos mode at r = keep = 1 vs the fp32 torch twin
+    (tolerance of tests/test_gpu_encoder.py: cos >= 0.999, rel. Frobenius <= 3e-2)."""
+    import paper_2605_17633_b200 as Z
+    from paper_2605_17633_b200.encoder import StripeSortEncoder
+    from paper_2605_17633_b200.weights import random_params
+
+    cfg = Z.EncoderConfig(grid=Z.GridShape(28, 28), d=320, heads=4, window=14, layout=("local", "global", "local"),
+                          r=1.0, keep_fraction=1.0)
+    params = random_params(cfg, DEV, seed=4, rel_pos=True, rel_pos_std=0.5)
+    assert params[0].bh is None and params[0].rel_pos_h.shape == (27, 80) and params[1].rel_pos_h.shape == (55, 80)
+    x = torch.randn(2, 28, 28, 320, device=DEV)
+    got = StripeSortEncoder(cfg, params)(x).double()
+    ref = _twin_blocks(x, params, cfg).double()
+    cos = float((got * ref).sum() / (got.norm() * ref.norm()))
+    assert cos >= 0.999 and rel(got, ref) <= 3e-2, (cos, rel(got, ref))
