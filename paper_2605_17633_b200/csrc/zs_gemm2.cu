@@ -219,10 +219,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
     const int q = warp & 3;          // TMEM lane quarter
     const int chalf = ew >> 2;       // column half of the 256-wide tile
     int it = 0;
+    // EPI 2: L2 prefetch of the residual rows this thread reads for a tile (one bulk prefetch of
+    // its half row), issued one tile ahead so the epilogue's read-modify-write hits L2 instead of
+    // waiting a DRAM round trip per 32-column chunk.  The row index is loaded at the top of the
+    // previous tile (volatile: kept there) so its latency hides behind that tile's epilogue.
+    auto res_row_of = [&](int tt, int& prow) -> bool {
+      const int pm = (tt / n_tiles) * 2 * BM + rank * BM + q * 32 + lane;
+      if (tt >= num_tiles || pm >= M || !ep.res) return false;
+      const int pn0 = (tt % n_tiles) * BN + chalf * (BN / 2);
+      if (pn0 >= N) return false;
+      prow = pm;
+      return true;
+    };
+    auto ld_row_v = [&](const int* p) {
+      int v;
+      asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+      return v;
+    };
+    auto prefetch_res = [&](int tt, int prow) {
+      const int pn0 = (tt % n_tiles) * BN + chalf * (BN / 2);
+      const int ncols = min(BN / 2, N - pn0);
+      const float* src = ep.res + (long long)prow * ep.ld_res + pn0;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(ncols * 4) : "memory");
+    };
+    auto res_row_index = [&](int tt, int pm) -> int {  // residual row of GEMM row pm (volatile loads)
+      if (ep.res_mod > 0) return pm % ep.res_mod;
+      if (ep.row_map) return ld_row_v(ep.row_map + pm);
+      return pm;
+    };
+    int pf_row = -1;  // residual row to prefetch for this cluster's next tile (-1: none)
+    if constexpr (EPI == 2) {
+      int pm;
+      if (res_row_of(cid, pm)) prefetch_res(cid, res_row_index(cid, pm));
+    }
     for (int t = cid; t < num_tiles; t += ncl, ++it) {
       const int as = it & 1;
       const int m0 = (t / n_tiles) * 2 * BM + rank * BM;
       const int n0 = (t % n_tiles) * BN;
+      if constexpr (EPI == 2) {
+        int pm;
+        pf_row = -1;
+        if (res_row_of(t + ncl, pm)) pf_row = res_row_index(t + ncl, pm);  // (zeroed rows: harmless)
+      }
       mbar_wait_sleep(&tfull[as], (it >> 1) & 1);
       tc_fence_after();
       const int m = m0 + q * 32 + lane;
@@ -235,6 +273,87 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
         if (ep.zero_rows) zero = ep.zero_rows[m] != 0;
       }
       const uint32_t trow = tmem_base + as * BN + ((uint32_t)(q * 32) << 16) + chalf * (BN / 2);
+      if constexpr (EPI == 2) {
+        // fp32 residual epilogue through a per-warp smem transpose: each lane moves 16-byte pieces
+        // so a warp instruction covers 4 full 128-byte row segments.  Rows are fixed per tile;
+        // the residual of chunk c + 1 is loaded while chunk c is transposed, added and stored.
+        float* xs = xstage + ew * 32 * XS;
+        const int c4 = lane & 7;  // float4 column within the 32-wide chunk
+        const int nbase = n0 + chalf * (BN / 2);
+        int orow2[8], rrow2[8];
+        bool live2[8], zero2[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int rl = 4 * i + (lane >> 3);
+          orow2[i] = __shfl_sync(0xffffffffu, (int)orow, rl);
+          rrow2[i] = __shfl_sync(0xffffffffu, (int)rrow, rl);
+          zero2[i] = __shfl_sync(0xffffffffu, (int)zero, rl) != 0;
+          live2[i] = m0 + q * 32 + rl < M;
+        }
+        auto load_res = [&](int c, float4(&xr)[8]) {
+          const int nb = nbase + c;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            xr[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (live2[i] && !zero2[i] && ep.res && nb < N) {
+              const float* src = ep.res + (long long)rrow2[i] * ep.ld_res + nb + 4 * c4;
+              asm volatile("ld.global.v4.f32 {%0, %1, %2, %3}, [%4];"
+                           : "=f"(xr[i].x), "=f"(xr[i].y), "=f"(xr[i].z), "=f"(xr[i].w)
+                           : "l"(src)
+                           : "memory");
+            }
+          }
+        };
+        float4 xa[8], xb[8];
+        load_res(0, xa);
+#pragma unroll 1
+        for (int c = 0; c < BN / 2; c += 32) {
+          if (c + 32 < BN / 2) load_res(c + 32, xb);
+          uint32_t r[32];
+          __syncwarp();
+          tmem_ld32(trow + c, r);
+          tmem_ld_wait();
+          const int nb = nbase + c;
+          {
+            float v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+            if (ep.bias && nb < N) {
+              const float4* b4 = reinterpret_cast<const float4*>(ep.bias + nb);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 b = __ldg(b4 + j);
+                v[4 * j] += b.x;
+                v[4 * j + 1] += b.y;
+                v[4 * j + 2] += b.z;
+                v[4 * j + 3] += b.w;
+              }
+            }
+            float4* xr = reinterpret_cast<float4*>(xs + lane * XS);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) xr[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (!live2[i] || nb >= N) continue;
+            const int rl = 4 * i + (lane >> 3);
+            float4 a = *reinterpret_cast<const float4*>(xs + rl * XS + 4 * c4);
+            if (zero2[i]) {
+              a = make_float4(0.f, 0.f, 0.f, 0.f);
+            } else {
+              a.x += xa[i].x;
+              a.y += xa[i].y;
+              a.z += xa[i].z;
+              a.w += xa[i].w;
+            }
+            reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.out) + (long long)orow2[i] * ep.ld_out + nb)[c4] = a;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) xa[i] = xb[i];
+        }
+      } else {
 #pragma unroll 1
       for (int c = 0; c < BN / 2; c += 32) {
         uint32_t r[32];
@@ -274,66 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
             }
           }
         }
-        if constexpr (EPI == 2) {
-          // fp32 residual epilogue through a per-warp smem transpose: each lane then moves
-          // 16-byte pieces so a warp instruction covers 4 full 128-byte row segments
-          float* xs = xstage + ew * 32 * XS;
-          {
-            float v[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-            if (ep.bias && nb < N) {
-              const float4* b4 = reinterpret_cast<const float4*>(ep.bias + nb);
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float4 b = __ldg(b4 + j);
-                v[4 * j] += b.x;
-                v[4 * j + 1] += b.y;
-                v[4 * j + 2] += b.z;
-                v[4 * j + 3] += b.w;
-              }
-            }
-            float4* xr = reinterpret_cast<float4*>(xs + lane * XS);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) xr[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          }
-          __syncwarp();
-          const int c4 = lane & 7;  // float4 column within the 32-wide chunk
-          // all 8 row groups in flight at once: rows, residual loads, then adds and stores
-          int orow2[8], rrow2[8];
-          bool live2[8], zero2[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int rl = 4 * i + (lane >> 3);
-            orow2[i] = __shfl_sync(0xffffffffu, (int)orow, rl);
-            rrow2[i] = __shfl_sync(0xffffffffu, (int)rrow, rl);
-            zero2[i] = __shfl_sync(0xffffffffu, (int)zero, rl) != 0;
-            live2[i] = (m0 + q * 32 + rl < M) && (nb < N);
-          }
-          float4 xres[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            xres[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (live2[i] && !zero2[i] && ep.res)
-              xres[i] = reinterpret_cast<const float4*>(ep.res + (long long)rrow2[i] * ep.ld_res + nb)[c4];
-          }
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (!live2[i]) continue;
-            const int rl = 4 * i + (lane >> 3);
-            float4 a = *reinterpret_cast<const float4*>(xs + rl * XS + 4 * c4);
-            if (zero2[i]) {
-              a = make_float4(0.f, 0.f, 0.f, 0.f);
-            } else {
-              a.x += xres[i].x;
-              a.y += xres[i].y;
-              a.z += xres[i].z;
-              a.w += xres[i].w;
-            }
-            reinterpret_cast<float4*>(reinterpret_cast<float*>(ep.out) + (long long)orow2[i] * ep.ld_out + nb)[c4] = a;
-          }
-          __syncwarp();
-        }
+      }
       }
       __syncwarp();
       tc_fence_before();
@@ -341,6 +401,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
         mbar_arrive(&tempty[as]);
       else
         mbar_arrive_remote(&tempty[as], 0);
+      if constexpr (EPI == 2) {
+        if (pf_row >= 0) prefetch_res(t + ncl, pf_row);
+      }
     }
   }
   tc_fence_before();

@@ -13,7 +13,7 @@ libs = {name: ctypes.CDLL(str(Path(_lib.LIB_PATH).parent / f)) for name, f in
 for l in libs.values():
     l.zs_gemm_bf16.argtypes = _lib.SIGNATURES["zs_gemm_bf16"]
 dev = "cuda"
-M = 16 * 4900
+M = (int(sys.argv[1]) if len(sys.argv) > 1 else 16) * 4900
 C = 1280
 a = torch.randn(M, C, device=dev).bfloat16()
 wq = (torch.randn(3 * C, C, device=dev) / 36).bfloat16()
@@ -36,6 +36,9 @@ def call(lib, kind):
     if kind == "proj":
         lib.zs_gemm_bf16(2, P(a), C, P(wp), C, M, C, C, None, P(x), C, P(x), C, None, None, 0, None, st)
         return 2.0 * M * C * C
+    if kind == "proj16":  # same shape, bf16 output (no fp32 residual traffic)
+        lib.zs_gemm_bf16(0, P(a), C, P(wp), C, M, C, C, None, P(out), C, None, 0, None, None, 0, None, st)
+        return 2.0 * M * C * C
     if kind == "fc1":
         lib.zs_gemm_bf16(1, P(a), C, P(w1), C, Mk, 4 * C, C, None, P(hid), 4 * C, None, 0, None, None, 0, None, st)
         return 2.0 * Mk * 4 * C * C
@@ -45,7 +48,7 @@ def call(lib, kind):
 
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for rnd in range(3):
-    for kind in ("qkv", "proj", "fc1", "fc2"):
+    for kind in (sys.argv[2].split(",") if len(sys.argv) > 2 else ("qkv", "proj", "proj16", "fc1", "fc2")):
         for name, lib in libs.items():
             for _ in range(2):
                 call(lib, kind)
