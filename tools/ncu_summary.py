@@ -51,7 +51,7 @@ def summarize(rep: str) -> list[dict]:
             if name.endswith("_mb"):
                 f = f * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(unit, 1.0)
             if name == "duration_us":
-                f = f * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1.0)
+                f = f * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0)
             rec[name] = round(f, 3)
         stalls = [(h.replace("smsp__pcsamp_warps_issue_stalled_", ""), float(v.replace(",", "")))
                   for h, v in d.items()

@@ -14,3 +14,6 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:zs_g
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:zs_attn -c 2 -o gpurun_out/attn_full -f \
     python tools/attn_prof.py both > /dev/null 2>&1; echo "ncu attn rc=$?"
 ls -la gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"zs_gemm2|zs_attn_win|zs_attn_glob" -s 3 -c 6 \
+    -o gpurun_out/bench_full -f python bench.py --profile --steps 1 --warmup 1 > /dev/null 2>&1; echo "ncu bench_full rc=$?"
+ls -la gpurun_out
