@@ -12,15 +12,15 @@
 // B200 design: the 2(2w-1) dot products of every (row, head) are ONE tcgen05 GEMM tile
 // D[128 rows, NB] = Q[128, dh] . R^T with R = [rel_pos_h ; rel_pos_w] (bf16, K-major, resident
 // in shared memory for the whole kernel), NB = 64 (w = 14) or 256 (w = 64) TMEM columns,
-// double-buffered.  The epilogue picks each row's w + w entries out of its 2(2w - 1)
+// one accumulator per epilogue warpgroup (4 for NB = 64, 2 otherwise).  The epilogue picks each row's w + w entries out of its 2(2w - 1)
 // (a per-row shift by qy / qx: fp16 row staged in shared memory, read back at the row's
 // offset) and writes
 //   mode 0: the attention kernels' fp16 operand row  [bh/tau | 0 | bw/tau | 0]  (2 * ceil16(w)
 //           halves) at btab[u * btab_us + (h * S + s) * W16]  (zs_attn_win.cu / zs_attn_glob.cu
 //           consume it directly: no fp32 table round trip)
 //   mode 1: fp32 bh, bw [units, heads, S, w] (reference BiasTables layout, unscaled)
-// Roles: warp 0 TMA (Q tiles, 4-stage ring; R once), warp 1 MMA, warps 2-5 epilogue (TMEM lane
-// quarter = warp % 4, one row per thread).
+// Roles: warp 0 TMA (Q tiles, 2-4 stage ring; R once), warp 1 MMA, warps 2.. epilogue
+// warpgroups (TMEM lane quarter = warp % 4, one row per thread; WG e takes every NE-th tile).
 #include <cuda_fp16.h>
 
 #include "zs_common.cuh"
@@ -29,9 +29,16 @@
 namespace zs {
 namespace relpos {
 
-constexpr int kThreads = 192;
-constexpr int kStages = 4;
 constexpr int BM = 128;
+// epilogue warpgroups (= TMEM accumulators; WG e takes the tiles k with k % NE == e) and
+// Q-tile ring depth per accumulator width: the epilogue (row shift through shared memory)
+// is the longer stage, so narrow tiles get more epilogue warpgroups
+__host__ __device__ constexpr int n_epi(int nb) { return nb <= 64 ? 4 : 2; }
+__host__ __device__ constexpr int n_stages(int nb) { return nb >= 256 ? 2 : 4; }
+__host__ __device__ constexpr int n_threads(int nb) { return 64 + 128 * n_epi(nb); }
+__host__ __device__ constexpr int tmem_cols(int nb) {
+  return n_epi(nb) * nb <= 32 ? 32 : (n_epi(nb) * nb <= 64 ? 64 : (n_epi(nb) * nb <= 128 ? 128 : (n_epi(nb) * nb <= 256 ? 256 : 512)));
+}
 
 struct Params {
   int units, heads, S, w, nr, nrb, tiles;
@@ -61,21 +68,22 @@ __global__ void relpos_table_kernel(const float* __restrict__ rh, const float* _
 }  // namespace relpos
 
 template <int DH, int NB, int MODE>
-__global__ void __launch_bounds__(relpos::kThreads, 1)
+__global__ void __launch_bounds__(relpos::n_threads(NB), 1)
     zs_relpos_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tq_t,
                      const __grid_constant__ CUtensorMap tr, const __grid_constant__ CUtensorMap tr_t,
                      const relpos::Params P) {
   using namespace relpos;
   constexpr bool kTail = DH == 80;
+  constexpr int NE = n_epi(NB), kStages = n_stages(NB), kCols = tmem_cols(NB);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + P.off_bar);
   uint64_t* a_full = bar;               // [kStages]
   uint64_t* a_empty = bar + kStages;    // [kStages]
   uint64_t* b_full = bar + 2 * kStages;
-  uint64_t* acc_full = b_full + 1;      // [2]
-  uint64_t* acc_empty = b_full + 3;     // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_full + 5);
+  uint64_t* acc_full = b_full + 1;        // [NE]
+  uint64_t* acc_empty = b_full + 1 + NE;  // [NE]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(b_full + 1 + 2 * NE);
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
 
   if (warp == 0 && lane == 0) {
@@ -84,13 +92,13 @@ __global__ void __launch_bounds__(relpos::kThreads, 1)
       mbar_init(&a_empty[s], 1);
     }
     mbar_init(b_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NE; ++s) {
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], 4);
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 2 * NB < 32 ? 32 : 2 * NB);
+  if (warp == 2) tmem_alloc(tmem_slot, kCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -120,8 +128,8 @@ __global__ void __launch_bounds__(relpos::kThreads, 1)
     mbar_wait(b_full, 0);
     int k = 0;
     for (int t = blockIdx.x; t < P.tiles; t += gridDim.x, ++k) {
-      const int s = k % kStages, buf = k & 1;
-      mbar_wait(&acc_empty[buf], ((k >> 1) & 1) ^ 1);
+      const int s = k % kStages, buf = k % NE;
+      mbar_wait(&acc_empty[buf], ((k / NE) & 1) ^ 1);
       mbar_wait(&a_full[s], (k / kStages) & 1);
       tc_fence_after();
       const uint32_t d = tmem + buf * NB;
@@ -133,20 +141,20 @@ __global__ void __launch_bounds__(relpos::kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue: one row per thread
-    const int qd = warp & 3;
+    const int qd = warp & 3, e = (warp - 2) >> 2;
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-    uint32_t* stage = reinterpret_cast<uint32_t*>(smem + P.off_stage) + (qd * 32 + lane) * P.stage_words;
+    uint32_t* stage = reinterpret_cast<uint32_t*>(smem + P.off_stage) + (e * BM + qd * 32 + lane) * P.stage_words;
     const __half* st16 = reinterpret_cast<const __half*>(stage);
     const int w = P.w, nr = P.nr;
-    int k = 0;
-    for (int t = blockIdx.x; t < P.tiles; t += gridDim.x, ++k) {
+    int j = 0;  // tiles taken by this warpgroup
+    for (int t = blockIdx.x + e * gridDim.x; t < P.tiles; t += NE * gridDim.x, ++j) {
       const int h = t % P.heads, rb = (t / P.heads) % P.nrb, u = t / (P.heads * P.nrb);
-      const int buf = k & 1;
+      const int buf = e;
       const int row = rb * BM + qd * 32 + lane;
       const bool valid = row < P.S;
       const int s = valid ? __ldg(P.q_sp + (long long)u * P.S + row) : 0;
       const int qy = (int)__umulhi((uint32_t)s, P.w_magic), qx = s - qy * w;
-      mbar_wait(&acc_full[buf], (k >> 1) & 1);
+      mbar_wait(&acc_full[buf], j & 1);
       tc_fence_after();
       const uint32_t acc = tmem + buf * NB + lane_off;
       if constexpr (MODE == 0) {
@@ -227,7 +235,7 @@ __global__ void __launch_bounds__(relpos::kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem, 2 * NB < 32 ? 32 : 2 * NB);
+  if (warp == 2) tmem_dealloc(tmem, kCols);
 }
 
 // Host launcher (internal).  mode 0 -> fp16 operand rows of w16 halves (bh/tau at [0, w),
@@ -275,10 +283,10 @@ int launch_relpos(const void* q, long long ldq, long long qus, int units, int he
   p.off_b = take(nb * 128, 1024);
   p.off_bt = take(nb * 32, 1024);
   p.a_stage = (BM * 128 + BM * 32 + 1023) / 1024 * 1024;
-  p.off_a = take(kStages * p.a_stage, 1024);
+  p.off_a = take(n_stages(nb) * p.a_stage, 1024);
   p.off_at = p.off_a + BM * 128;
   p.stage_words = mode == 0 ? nb / 2 + 4 : 0;
-  p.off_stage = take(BM * p.stage_words * 4, 16);
+  p.off_stage = take(n_epi(nb) * BM * p.stage_words * 4, 16);
   p.off_bar = take(256, 8);
   const size_t smem = 1024 + (size_t)off;
   if (smem > 227 * 1024) return 1;
@@ -303,7 +311,7 @@ int launch_relpos(const void* q, long long ldq, long long qus, int units, int he
   if (grid > p.tiles) grid = p.tiles;
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, kThreads, smem, st>>>(m[0], m[1], m[2], m[3], p);
+    kern<<<grid, n_threads(nb), smem, st>>>(m[0], m[1], m[2], m[3], p);
   };
 #define ZS_RELPOS_DISPATCH(D)                                                          \
   if (nb == 64) {                                                                      \
