@@ -459,14 +459,18 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
     const unsigned dead = warp_live ? (P.uni[X] & ~live) : 0u;
     const float cexp = P.tau * 1.4426950408889634f;  // logit = tau * S'; exp via 2^(S' tau log2e)
 
-    auto epilogue = [&](int it, float inv) {
+    // output row of (item, row): o_rows entry loaded when the item starts (om), consumed by its
+    // epilogue one item later, so the load latency is off the epilogue's path
+    auto out_row = [&](int it) -> int {
+      return (valid && P.o_rows) ? __ldg(P.o_rows + (long long)(it / P.heads) * P.S + row) : 0;
+    };
+    auto epilogue = [&](int it, float inv, int om) {
       const int u = it / P.heads, h = it % P.heads;
       long long orow_off = (long long)u * P.o_unit_stride + (long long)row * P.ldo;
       bool ok = valid;
       if (ok && P.o_rows) {
-        const int m = P.o_rows[(long long)u * P.S + row];
-        ok = m >= 0;
-        orow_off = (long long)m * P.ldo;
+        ok = om >= 0;
+        orow_off = (long long)om * P.ldo;
       }
       __nv_bfloat16* dst = P.out + orow_off + h * DH;
       // 16-byte stores (measured faster here than 32-byte st.global.v8: tools/attn_ab.py)
@@ -511,10 +515,11 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
     };
 
     int k = 0;
-    int prev_it = -1;
+    int prev_it = -1, prev_om = 0;
     float prev_inv = 0.f;
     for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
       if (warp_live) {
+        const int om = out_row(it);
         mbar_wait(&s_full[X], k & 1);
         tc_fence_after();
         if (lane == 0) ZS_TR(k, 16 + 8 * X + 2);
@@ -565,10 +570,11 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         if (prev_it >= 0) {
           mbar_wait(&o_full[X], (k - 1) & 1);
           tc_fence_after();
-          epilogue(prev_it, prev_inv);
+          epilogue(prev_it, prev_inv, prev_om);
           if (lane == 0) ZS_TR(k, 16 + 8 * X + 4);
         }
         prev_it = it;
+        prev_om = om;
         prev_inv = 1.0f / rs;
         tc_fence_before();
         __syncwarp();
@@ -581,7 +587,7 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
     if (warp_live && prev_it >= 0) {
       mbar_wait(&o_full[X], (k - 1) & 1);
       tc_fence_after();
-      epilogue(prev_it, prev_inv);
+      epilogue(prev_it, prev_inv, prev_om);
     }
   }
   tc_fence_before();

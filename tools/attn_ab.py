@@ -16,6 +16,8 @@ libs = {name: ctypes.CDLL(str(Path(_lib.LIB_PATH).parent / f)) for name, f in
         [("new", "libzstripe_b200.so"), ("old", "libzstripe_b200_old.so")]}
 for l in libs.values():
     l.zs_stripe_attn_fwd.argtypes = _lib.SIGNATURES["zs_stripe_attn_fwd"]
+    l.zs_stripe_attn_fwd_rows.argtypes = _lib.SIGNATURES["zs_stripe_attn_fwd_rows"]
+ROWS = "rows" in sys.argv  # compacted output rows (the encoder's pad-skipping path): 16 % of rows dropped
 kind = sys.argv[1] if len(sys.argv) > 1 else "local"
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 H, dh = 16, 80
@@ -31,8 +33,21 @@ outs = {n: torch.empty(U * S, C, device="cuda", dtype=torch.bfloat16) for n in l
 st = torch.cuda.current_stream().cuda_stream
 
 
+orows = None
+if ROWS:
+    keep = torch.rand(U * S, device="cuda") > 0.16
+    orows = torch.where(keep, torch.cumsum(keep.int(), 0) - 1, torch.full_like(keep, -1, dtype=torch.long)).int()
+
+
 def call(lib, out):
     q = qkv
+    if ROWS:
+        rc = lib.zs_stripe_attn_fwd_rows(q.data_ptr(), q.data_ptr() + 2 * C, q.data_ptr() + 4 * C, 3 * C, 3 * C,
+                                         3 * C, S * 3 * C, S * 3 * C, U, H, S, S, dh, bh.data_ptr(), bw.data_ptr(), w,
+                                         sp.data_ptr(), sp.data_ptr(), tile, tile, p, dh ** -0.5, out.data_ptr(), C,
+                                         S * C, orows.data_ptr(), st)
+        assert rc == 0, rc
+        return
     rc = lib.zs_stripe_attn_fwd(q.data_ptr(), q.data_ptr() + 2 * C, q.data_ptr() + 4 * C, 3 * C, 3 * C, 3 * C,
                                 S * 3 * C, S * 3 * C, U, H, S, S, dh, bh.data_ptr(), bw.data_ptr(), w, sp.data_ptr(),
                                 sp.data_ptr(), tile, tile, p, dh ** -0.5, out.data_ptr(), C, S * C, st)
