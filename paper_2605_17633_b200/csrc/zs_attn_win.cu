@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         if (lane == 0) ZS_TR(k, 2);
         if (nt > 1) {
           if (k > 0) {  // PV of tile B, previous item
-            mbar_wait(&p_full[1], (k - 1) & 1);
+            mbar_wait_sleep(&p_full[1], (k - 1) & 1);
             tc_fence_after();
             issue_pv(1, pb);
             umma_commit_elect(&v_empty[pb]);
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         }
         umma_commit_elect(&qk_empty[b]);
         umma_commit_elect(bk_empty);
-        mbar_wait(&p_full[0], k & 1);
+        mbar_wait_sleep(&p_full[0], k & 1);
         mbar_wait(&v_full[b], (k >> 1) & 1);
         tc_fence_after();
         issue_pv(0, b);

@@ -1,3 +1,2 @@
 timeout 300 python -m pytest tests/test_gpu_kernels.py -q -x -k "attention" --timeout 120 2>&1 | tail -2
 timeout 100 python tools/attn_ab.py local 64 rows 2>&1 | tail -7
-timeout 100 python tools/attn_ab.py global 64 rows 2>&1 | tail -7
