@@ -355,45 +355,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
         }
       } else {
 #pragma unroll 1
-      for (int c = 0; c < BN / 2; c += 32) {
-        uint32_t r[32];
-        __syncwarp();
-        tmem_ld32(trow + c, r);
-        tmem_ld_wait();
-        const int nb = n0 + chalf * (BN / 2) + c;
-        if (valid && nb < N) {
-          float v[32];
+        for (int c = 0; c < BN / 2; c += 32) {
+          uint32_t r[32];
+          __syncwarp();
+          tmem_ld32(trow + c, r);
+          tmem_ld_wait();
+          const int nb = n0 + chalf * (BN / 2) + c;
+          if (valid && nb < N) {
+            float v[32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          if (ep.bias) {
-            const float4* b4 = reinterpret_cast<const float4*>(ep.bias + nb);
+            for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+            if (ep.bias) {
+              const float4* b4 = reinterpret_cast<const float4*>(ep.bias + nb);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 b = __ldg(b4 + j);
-              v[4 * j] += b.x;
-              v[4 * j + 1] += b.y;
-              v[4 * j + 2] += b.z;
-              v[4 * j + 3] += b.w;
+              for (int j = 0; j < 8; ++j) {
+                const float4 b = __ldg(b4 + j);
+                v[4 * j] += b.x;
+                v[4 * j + 1] += b.y;
+                v[4 * j + 2] += b.z;
+                v[4 * j + 3] += b.w;
+              }
             }
-          }
-          if constexpr (EPI == 0 || EPI == 1) {
-            if constexpr (EPI == 1) {
+            if constexpr (EPI == 0 || EPI == 1) {
+              if constexpr (EPI == 1) {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
-            }
-            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(ep.out) + orow * ep.ld_out + nb);
+                for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+              }
+              uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(ep.out) + orow * ep.ld_out + nb);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              uint4 w;
-              w.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
-              w.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
-              w.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
-              w.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
-              dst[j] = w;
+              for (int j = 0; j < 4; ++j) {
+                uint4 w;
+                w.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
+                w.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
+                w.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
+                w.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
+                dst[j] = w;
+              }
             }
           }
         }
-      }
       }
       __syncwarp();
       tc_fence_before();
