@@ -219,13 +219,22 @@ def test_rank_ties_and_nan_follow_numpy_lexsort():
 
 
 # ---------------------------------------------------------------- attention
-def _attn_case(units, heads, S, dh, w, tile, r, seed=0, bscale=0.5):
+def _parity_stripes(S, w, g):
+    """σ as the global stripe-sort produces it for G = 4: the four (y % 2, x % 2) classes one after
+    the other (stripesort.py:38-62 over 2x2 Morton groups), each in its own order."""
+    pos = torch.arange(S)
+    cls = ((pos // w) % 2) * 2 + (pos % w) % 2
+    return torch.argsort(cls.double() * 2 + torch.rand(S, generator=g, dtype=torch.float64))
+
+
+def _attn_case(units, heads, S, dh, w, tile, r, seed=0, bscale=0.5, stripes=False):
     g = torch.Generator().manual_seed(seed)
     C = heads * dh
     qkv = torch.randn(units * S, 3 * C, generator=g).bfloat16().to(DEV)
     bh = (bscale * torch.randn(heads, S, w, generator=g)).to(DEV)
     bw = (bscale * torch.randn(heads, S, w, generator=g)).to(DEV)
-    sp = torch.stack([torch.randperm(S, generator=g) for _ in range(units)]).int().to(DEV)
+    mk = (lambda: _parity_stripes(S, w, g)) if stripes else (lambda: torch.randperm(S, generator=g))
+    sp = torch.stack([mk() for _ in range(units)]).int().to(DEV)
     T = -(-S // tile)
     out = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], units=units, heads=heads, sq=S, sk=S, dh=dh,
                         bh=bh, bw=bw, q_sp=sp, k_sp=sp, b_row=tile, b_col=tile, prefix=math.floor(r * T),
@@ -280,6 +289,15 @@ def test_attention_window_kernels_agree(r, monkeypatch):
 @pytest.mark.parametrize("r", [0.2, 0.4, 1.0])
 def test_attention_global(dh, r):
     assert _attn_case(2, 2, 4096, dh, 64, 128, r) < 1e-2
+
+
+@pytest.mark.parametrize("dh", [64, 80])
+@pytest.mark.parametrize("r", [0.2, 0.4, 1.0])
+def test_attention_global_parity_stripes(dh, r):
+    """Stripe-ordered keys as the global stripe sort produces them (every 128-key chunk inside one
+    (y % 2, x % 2) class), 4096- and 1024-token grids."""
+    assert _attn_case(2, 2, 4096, dh, 64, 128, r, seed=8, stripes=True) < 1e-2
+    assert _attn_case(3, 2, 1024, dh, 32, 128, r, seed=9, stripes=True) < 1e-2
 
 
 @pytest.mark.parametrize("S,w,tile", [(4096, 64, 128), (196, 14, 32)])

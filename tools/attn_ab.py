@@ -29,6 +29,11 @@ qkv = torch.randn(U * S, 3 * C, device="cuda").bfloat16()
 bh = torch.randn(H, S, w, device="cuda") * 0.5
 bw = torch.randn(H, S, w, device="cuda") * 0.5
 sp = torch.argsort(torch.rand(U, S, device="cuda"), dim=1).int().contiguous()
+if "stripes" in sys.argv:  # σ made of the 4 (y % 2, x % 2) parity classes, each shuffled (global stripes)
+    pos = torch.arange(S, device="cuda")
+    cls = ((pos // w) % 2) * 2 + (pos % w) % 2
+    key = cls[None, :].float() * 2 + torch.rand(U, S, device="cuda")
+    sp = torch.argsort(key, dim=1).int().contiguous()
 outs = {n: torch.empty(U * S, C, device="cuda", dtype=torch.bfloat16) for n in libs}
 st = torch.cuda.current_stream().cuda_stream
 
