@@ -159,8 +159,8 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
   uint64_t* v_full = bar + 16;   // [VST]
   uint64_t* v_empty = bar + 20;  // [VST]
   uint64_t* s_full = bar + 24;   // [wg]
-  uint64_t* p_full = bar + 26;   // [wg]  4 warps: P of the chunk in TMEM
-  uint64_t* o_full = bar + 28;   // [wg]  PV of the chunk completed
+  uint64_t* p_full = bar + 26;   // [S buffer]  8 softmax warps: P of the chunk in TMEM
+  uint64_t* o_full = bar + 28;   // PV of a chunk completed (one completion per chunk)
   uint64_t* o_free = bar + 30;   // 8 warps: O_0 / O_1 read by the item's epilogue
   uint64_t* bq_full = bar + 31;  // 8 warps: the item's Bq rows are in TMEM
   uint64_t* bq_free = bar + 32;  // the item's last S' completed (Bq may be replaced)
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 4);
+      mbar_init(&p_full[s], 8);
       mbar_init(&o_full[s], 1);
     }
     for (int s = 0; s < KST; ++s) {
@@ -291,14 +291,14 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         tc_fence_after();
         const uint64_t v = dv + vs * TILE16, vt = dvt + vs * TILE16;
         const uint32_t a0 = tmem + TM_S + w * 128;
-        const uint32_t d = tmem + TM_O + w * 80;
+        const uint32_t d = tmem + TM_O;
 #pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks) {
           const uint32_t acc = (!first || ks > 0) ? 1u : 0u;
           umma_ts(d, a0 + 8 * ks, v + ks * (16 * 128 / 16), id_pv, acc);
           if constexpr (kTail) umma_ts(d + 64, a0 + 8 * ks, vt + ks * (16 * 32 / 16), id_pv2, acc);
         }
-        umma_commit_elect(&o_full[w]);
+        umma_commit_elect(o_full);
         umma_commit_elect(&v_empty[vs]);
       };
       // PV(c-1) is issued right after S'(c): S'(c) goes to the other WG's S buffer, and S'(c)
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
           pend_c = c;
           pend_w = w;
           pend_k = k;
-          pend_first = j < 2;  // first chunk of WG w in this item: O_w starts fresh
+          pend_first = j == 0;  // first chunk of the item: O starts fresh
         }
         // the item's last PV now: its epilogue (and with it the next item's Bq install, which
         // the next S' waits for) depends on it
@@ -429,35 +429,53 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
     // ------------------------------------------------------------ softmax warpgroups
-    const int w = (warp - 4) >> 2;  // WG: chunk ordinals with c % 2 == w
+    // every chunk is processed by all 8 softmax warps: warp (half w, quarter wq) owns rows
+    // wq*32 + lane (TMEM lane quarter) and key columns [64w, 64w + 64) of the chunk; the two
+    // halves of a row exchange their partial max through shared memory (pair barrier 1 + wq)
+    // and keep partial row sums, merged once per item.  One O accumulator: half w rescales /
+    // reads O columns [40w, 40w + 40).
+    const int w = (warp - 4) >> 2;
     const int wq = warp & 3;
-    const int r = wq * 32 + lane;   // row within the tile == TMEM lane
+    const int r = wq * 32 + lane;  // row within the tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    const uint32_t s_addr = tmem + TM_S + w * 128 + lane_off;
-    const uint32_t o_addr = tmem + TM_O + w * 80 + lane_off;
-    const uint32_t o_oth = tmem + TM_O + (w ^ 1) * 80 + lane_off;
-    const uint32_t bq_addr = tmem + TM_BQ + w * 32 + lane_off;  // this WG's 64 fp16 bias columns
-    float* ml = reinterpret_cast<float*>(smem + P.off_ml);  // [item parity][2 wg][2][BQ]: m, l
+    const uint32_t o_addr = tmem + TM_O + lane_off;
+    const uint32_t bq_addr = tmem + TM_BQ + w * 32 + lane_off;  // this half's 64 fp16 bias columns
+    float* xch = reinterpret_cast<float*>(smem + P.off_ml);     // [chunk parity][half][BQ] partial max
+    float* lx = xch + 4 * BQ;                                   // [half][BQ] partial row sums
+    const uint32_t pair_bar = 1 + wq;
     constexpr float L2E = 1.4426950408889634f;
     constexpr float kThr = 5.545177444479562f;  // ln 256
     const float tau = P.tau, cexp = P.tau * L2E;
 
-    // Bq rows of item `it2` (this WG's half: 64 fp16 = 128 bytes) -> TMEM, once the previous
-    // item's last S' has completed (bq_free)
-    auto install_bq = [&](int it2, int k2) {
-      uint4 x[8];
-      const int i2 = it2 % nmb, uh2 = it2 / nmb, h2 = uh2 % P.heads, u2 = uh2 / P.heads;
+    // Bq rows of item `it2` (this half: 64 fp16 = 128 bytes): loaded one item ahead (volatile
+    // loads stay where they are issued), written into TMEM once the previous item's last S' has
+    // completed (bq_free).  The item boundary then waits on no global-memory latency.
+    // spatial position of this thread's query row in item it2 (volatile load: issued here,
+    // consumed one item later)
+    auto load_sp = [&](int it2) -> int {
+      const int i2 = it2 % nmb, u2 = it2 / nmb / P.heads;
       const int row2 = i2 * BQ + r;
-      if (row2 < P.S) {
-        const int sp = __ldg(P.q_sp + (long long)u2 * P.S + row2);
-        const uint4* src = reinterpret_cast<const uint4*>(P.btab + (long long)u2 * P.btab_us +
-                                                      ((long long)h2 * P.S + sp) * 128 + w * 64);
+      int v = 0;
+      if (it2 < P.items && row2 < P.S)
+        asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(P.q_sp + (long long)u2 * P.S + row2) : "memory");
+      return v;
+    };
+    auto load_bq = [&](int it2, int sp, uint4 (&x)[8]) {
+      const int i2 = it2 % nmb, uh2 = it2 / nmb, h2 = uh2 % P.heads, u2 = uh2 / P.heads;
+      const bool ok = it2 < P.items && i2 * BQ + r < P.S;
+      const uint4* src = reinterpret_cast<const uint4*>(P.btab + (long long)u2 * P.btab_us +
+                                                    ((long long)h2 * P.S + sp) * 128 + w * 64);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) x[q] = __ldg(src + q);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) x[q] = make_uint4(0u, 0u, 0u, 0u);
+      for (int q = 0; q < 8; ++q) {
+        x[q] = make_uint4(0u, 0u, 0u, 0u);
+        if (ok)
+          asm volatile("ld.global.nc.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(x[q].x), "=r"(x[q].y), "=r"(x[q].z), "=r"(x[q].w)
+                       : "l"(src + q)
+                       : "memory");
       }
+    };
+    auto store_bq = [&](const uint4 (&x)[8], int k2) {
       uint32_t v[32];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
@@ -474,112 +492,120 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(bq_full);
     };
+    // O columns of this half: [40w, 40w + 32) and [40w + 32, 40w + 40) (dh = 80), or
+    // [32w, 32w + 32) (dh = 64)
+    constexpr int OH = DH / 2;
+    auto o_scale = [&](float alpha) {
+      uint32_t pr[32];
+      tmem_ld32(o_addr + w * OH, pr);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 32; ++q) pr[q] = __float_as_uint(__uint_as_float(pr[q]) * alpha);
+      tmem_st32(o_addr + w * OH, pr);
+      if constexpr (OH == 40) {
+        uint32_t p8[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(p8[0]), "=r"(p8[1]), "=r"(p8[2]), "=r"(p8[3]), "=r"(p8[4]), "=r"(p8[5]),
+                       "=r"(p8[6]), "=r"(p8[7])
+                     : "r"(o_addr + w * OH + 32));
+        tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) p8[q] = __float_as_uint(__uint_as_float(p8[q]) * alpha);
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(o_addr + w * OH + 32),
+                     "r"(p8[0]), "r"(p8[1]), "r"(p8[2]), "r"(p8[3]), "r"(p8[4]), "r"(p8[5]), "r"(p8[6]), "r"(p8[7])
+                     : "memory");
+      }
+    };
 
-    install_bq(blockIdx.x, 0);
-    int k = 0, c = 0, nsw = 0;  // nsw: chunks this WG processed (phase of s_full / o_full)
+    const int G = gridDim.x;
+    uint4 bqx[8];
+    load_bq(blockIdx.x, load_sp(blockIdx.x), bqx);
+    store_bq(bqx, 0);
+    load_bq(blockIdx.x + G, load_sp(blockIdx.x + G), bqx);  // next item's rows, in flight during this item
+    int sp_nn = load_sp(blockIdx.x + 2 * G);                  // and the row index of the one after
+    int k = 0, c = 0;
     for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
       const int i = it % nmb, uh = it / nmb, h = uh % P.heads, u = uh / P.heads;
       const int nc = n_chunks(P, i);
       const int row = i * BQ + r;
       if (lane == 0 && wq == 0) ZG_TR(k, 2 + w);
       float m_ref = -INFINITY, ell = 0.f;
-      int mine = 0;  // chunks of this item processed by this WG
       for (int j = 0; j < nc; ++j, ++c) {
-        if ((c & 1) != w) continue;
+        const int buf = c & 1;
         const int cj = chunk_of(P, i, j);
-        const int kvalid = P.S - cj * BQ;  // keys of this chunk below S
-        mbar_wait(&s_full[w], nsw & 1);
+        const int kvalid = P.S - cj * BQ - 64 * w;  // keys of this half below S
+        mbar_wait(&s_full[buf], (c >> 1) & 1);
         tc_fence_after();
-        if (lane == 0 && wq == 0 && mine == 0 && w == 0) ZG_TR(k, 0);
-        if (lane == 0 && wq == 0) ZG_T2(k, j, 1);
-        uint32_t sr[128];
-#pragma unroll
-        for (int g = 0; g < 4; ++g) tmem_ld32(s_addr + 32 * g, *reinterpret_cast<uint32_t(*)[32]>(sr + 32 * g));
+        if (lane == 0 && wq == 0 && j == 0 && w == 0) ZG_TR(k, 0);
+        const uint32_t s_addr = tmem + TM_S + buf * 128 + lane_off;
+        uint32_t sr[64];
+        tmem_ld32(s_addr + 64 * w, *reinterpret_cast<uint32_t(*)[32]>(sr));
+        tmem_ld32(s_addr + 64 * w + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
         tmem_ld_wait();
-        if (kvalid < BQ) {
+        if (kvalid < 64) {
 #pragma unroll
-          for (int jj = 0; jj < 128; ++jj)
+          for (int jj = 0; jj < 64; ++jj)
             if (jj >= kvalid) sr[jj] = __float_as_uint(-INFINITY);
         }
         float m0 = __uint_as_float(sr[0]), m1 = __uint_as_float(sr[1]);
 #pragma unroll
-        for (int jj = 2; jj < 128; jj += 2) {
+        for (int jj = 2; jj < 64; jj += 2) {
           m0 = fmaxf(m0, __uint_as_float(sr[jj]));
           m1 = fmaxf(m1, __uint_as_float(sr[jj + 1]));
         }
-        const float mx = tau * fmaxf(m0, m1);  // max logit (tau > 0)
-        // lazy rescale: the reference max moves only past the threshold.  The O rescale is a
-        // warp-wide TMEM round trip (tcgen05.ld / st are .sync.aligned): taken when ANY row of
-        // the warp moves its reference, with alpha = 1 for the rows that do not
+        // partial max -> partner half; after this barrier both halves' S loads are complete,
+        // so P may overwrite S columns of either half
+        const float mp = fmaxf(m0, m1);
+        xch[(buf * 2 + w) * BQ + r] = mp;
+        tc_fence_before();
+        named_bar_sync(pair_bar, 64);
+        tc_fence_after();
+        const float mx = tau * fmaxf(mp, xch[(buf * 2 + (w ^ 1)) * BQ + r]);  // row max logit
+        // lazy rescale (identical decision in both halves): a warp-wide TMEM round trip when any
+        // row of the warp moves its reference, alpha = 1 for the others
         float alpha = 1.f;
         const bool upd = mx > m_ref + kThr || (m_ref == -INFINITY && mx > -INFINITY);
         if (upd) alpha = (m_ref == -INFINITY) ? 0.f : ex2((m_ref - mx) * L2E);
         if (__any_sync(0xffffffffu, upd)) {
-          if (mine > 0) {
-            // previous PV into O_w must have completed before O_w is rescaled
-            mbar_wait(&o_full[w], (nsw - 1) & 1);
+          if (j > 0) {
+            mbar_wait(o_full, (c - 1) & 1);  // PV(c - 1) complete before O is rescaled
             tc_fence_after();
-            uint32_t pr[32];
-            tmem_ld32(o_addr, pr);
-            tmem_ld_wait();
-#pragma unroll
-            for (int q = 0; q < 32; ++q) pr[q] = __float_as_uint(__uint_as_float(pr[q]) * alpha);
-            tmem_st32(o_addr, pr);
-            tmem_ld32(o_addr + 32, pr);
-            tmem_ld_wait();
-#pragma unroll
-            for (int q = 0; q < 32; ++q) pr[q] = __float_as_uint(__uint_as_float(pr[q]) * alpha);
-            tmem_st32(o_addr + 32, pr);
-            if constexpr (DH == 80) {
-              uint32_t p16[16];
-              tmem_ld16(o_addr + 64, p16);
-              tmem_ld_wait();
-#pragma unroll
-              for (int q = 0; q < 16; ++q) p16[q] = __float_as_uint(__uint_as_float(p16[q]) * alpha);
-              tmem_st16(o_addr + 64, p16);
-            }
+            o_scale(alpha);
           }
           if (upd) m_ref = mx;
         }
         const float mc = (m_ref == -INFINITY) ? 0.f : m_ref * L2E;
         float r0 = 0.f, r1 = 0.f;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
+        for (int g = 0; g < 2; ++g) {
           uint32_t pk[16];
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            float a, b;
+            float a, b2;
             ex2x2(fmaf(__uint_as_float(sr[32 * g + 2 * q]), cexp, -mc),
-                  fmaf(__uint_as_float(sr[32 * g + 2 * q + 1]), cexp, -mc), a, b);
+                  fmaf(__uint_as_float(sr[32 * g + 2 * q + 1]), cexp, -mc), a, b2);
             r0 += a;
-            r1 += b;
-            pk[q] = pack_bf16(a, b);
+            r1 += b2;
+            pk[q] = pack_bf16(a, b2);
           }
-          tmem_st16(s_addr + 16 * g, pk);
+          tmem_st16(s_addr + 32 * w + 16 * g, pk);  // P (bf16) of keys [64w + 32g, +32)
         }
         ell = ell * alpha + (r0 + r1);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[w]);
-        if (lane == 0 && wq == 0 && mine == 0 && w == 0) ZG_TR(k, 1);
-        if (lane == 0 && wq == 0) ZG_T2(k, j, 2);
-        ++nsw;
-        ++mine;
+        if (lane == 0) mbar_arrive(&p_full[buf]);
+        if (lane == 0 && wq == 0 && j == 0 && w == 0) ZG_TR(k, 1);
       }
-      // ---- item epilogue: merge the two WGs' partial softmaxes, each WG writes half the columns
-      float* mlk = ml + (k & 1) * 4 * BQ;
-      mlk[(w * 2 + 0) * BQ + r] = m_ref;
-      mlk[(w * 2 + 1) * BQ + r] = ell;
-      if (mine > 0) mbar_wait(&o_full[w], (nsw - 1) & 1);  // this WG's last PV
-      named_bar_sync(1, 256);  // both WGs: m / l posted, both last PVs complete
-      const float mo = mlk[((w ^ 1) * 2 + 0) * BQ + r], lo = mlk[((w ^ 1) * 2 + 1) * BQ + r];
-      const float mm = fmaxf(m_ref, mo);
-      const float a_me = (m_ref == -INFINITY) ? 0.f : ex2((m_ref - mm) * L2E);
-      const float a_ot = (mo == -INFINITY) ? 0.f : ex2((mo - mm) * L2E);
-      const float inv = 1.0f / (ell * a_me + lo * a_ot);
-      const float s_me = a_me * inv, s_ot = a_ot * inv;
+      // ---- item epilogue: row sum from both halves; each half writes its O columns
+      lx[w * BQ + r] = ell;
+      // the item's last PV(c - 1).  o_full completes once per chunk; parity waits are exact only
+      // one phase ahead, and s_full(c - 1) guaranteed PV(c - 3) only: wait PV(c - 2) first
+      mbar_wait(o_full, (c - 2) & 1);
+      mbar_wait(o_full, (c - 1) & 1);
+      named_bar_sync(pair_bar, 64);
       tc_fence_after();
+      const float inv = 1.0f / (ell + lx[(w ^ 1) * BQ + r]);
       bool valid = row < P.S;
       long long orow_off = (long long)u * P.o_unit_stride + (long long)row * P.ldo;
       if (valid && P.o_rows) {
@@ -587,42 +613,29 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         valid = m >= 0;
         orow_off = (long long)m * P.ldo;
       }
-      __nv_bfloat16* dst = P.out + orow_off + h * DH;
-      // WG0: columns [0, 32) (+ [64, 80) when dh = 80), WG1: [32, 64)
+      __nv_bfloat16* dst = P.out + orow_off + h * DH + w * OH;
       {
-        const uint32_t c0 = w * 32;
-        uint32_t a[32], b[32];
-        tmem_ld32(o_addr + c0, a);
-        tmem_ld32(o_oth + c0, b);
-        tmem_ld_wait();
-        if (valid) {
-          uint4 o4[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint32_t v[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e)  // a WG without chunks has a stale O: weight exactly 0
-              v[e] = __float_as_uint((s_me != 0.f ? __uint_as_float(a[8 * q + e]) * s_me : 0.f) +
-                                     (s_ot != 0.f ? __uint_as_float(b[8 * q + e]) * s_ot : 0.f));
-            o4[q] = scale_pack8(v, 1.f);
-          }
-          st_global_32B(dst + c0, o4[0], o4[1]);  // full 32-byte sectors
-          st_global_32B(dst + c0 + 16, o4[2], o4[3]);
-        }
-      }
-      if constexpr (DH == 80) {
-        if (w == 0) {
-          uint32_t a[16], b[16];
-          tmem_ld16(o_addr + 64, a);
-          tmem_ld16(o_oth + 64, b);
+        uint32_t a[32];
+        tmem_ld32(o_addr + w * OH, a);
+        if constexpr (OH == 40) {
+          uint32_t a8[8];
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(a8[0]), "=r"(a8[1]), "=r"(a8[2]), "=r"(a8[3]), "=r"(a8[4]), "=r"(a8[5]),
+                         "=r"(a8[6]), "=r"(a8[7])
+                       : "r"(o_addr + w * OH + 32));
           tmem_ld_wait();
           if (valid) {
-            uint32_t v[16];
+            uint4* d4 = reinterpret_cast<uint4*>(dst);  // 80-byte aligned row halves: 16-byte stores
 #pragma unroll
-            for (int e = 0; e < 16; ++e)
-              v[e] = __float_as_uint((s_me != 0.f ? __uint_as_float(a[e]) * s_me : 0.f) +
-                                     (s_ot != 0.f ? __uint_as_float(b[e]) * s_ot : 0.f));
-            st_global_32B(dst + 64, scale_pack8(v, 1.f), scale_pack8(v + 8, 1.f));
+            for (int q = 0; q < 4; ++q) d4[q] = scale_pack8(a + 8 * q, inv);
+            d4[4] = scale_pack8(a8, inv);
+          }
+        } else {
+          tmem_ld_wait();
+          if (valid) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d4[q] = scale_pack8(a + 8 * q, inv);
           }
         }
       }
@@ -631,7 +644,11 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       if (lane == 0) mbar_arrive(o_free);
       if (lane == 0 && wq == 0) ZG_TR(k, 4 + w);
       // next item's bias rows into TMEM once this item's last S' has completed
-      if (it + (int)gridDim.x < P.items) install_bq(it + gridDim.x, k + 1);
+      if (it + G < P.items) {
+        store_bq(bqx, k + 1);
+        load_bq(it + 2 * G, sp_nn, bqx);
+        sp_nn = load_sp(it + 3 * G);
+      }
     }
   }
   tc_fence_before();
