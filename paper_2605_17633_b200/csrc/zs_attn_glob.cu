@@ -537,6 +537,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         mbar_wait(&s_full[buf], (c >> 1) & 1);
         tc_fence_after();
         if (lane == 0 && wq == 0 && j == 0 && w == 0) ZG_TR(k, 0);
+        if (lane == 0 && wq == 0 && w == 0) ZG_T2(k, j, 1);
         const uint32_t s_addr = tmem + TM_S + buf * 128 + lane_off;
         uint32_t sr[64];
         tmem_ld32(s_addr + 64 * w, *reinterpret_cast<uint32_t(*)[32]>(sr));
@@ -575,27 +576,25 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
           if (upd) m_ref = mx;
         }
         const float mc = (m_ref == -INFINITY) ? 0.f : m_ref * L2E;
-        float r0 = 0.f, r1 = 0.f;
+        const unsigned long long c2 = f32x2(cexp, cexp), m2 = f32x2(-mc, -mc);
+        unsigned long long acc = f32x2(0.f, 0.f);
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           uint32_t pk[16];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            float a, b2;
-            ex2x2(fmaf(__uint_as_float(sr[32 * g + 2 * q]), cexp, -mc),
-                  fmaf(__uint_as_float(sr[32 * g + 2 * q + 1]), cexp, -mc), a, b2);
-            r0 += a;
-            r1 += b2;
-            pk[q] = pack_bf16(a, b2);
-          }
+          for (int q = 0; q < 16; ++q)
+            pk[q] = exp2_pair_bf16(__uint_as_float(sr[32 * g + 2 * q]), __uint_as_float(sr[32 * g + 2 * q + 1]), c2,
+                                   m2, acc);
           tmem_st16(s_addr + 32 * w + 16 * g, pk);  // P (bf16) of keys [64w + 32g, +32)
         }
-        ell = ell * alpha + (r0 + r1);
+        const float2 rs = unpack_f32x2(acc);
+        ell = ell * alpha + (rs.x + rs.y);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[buf]);
         if (lane == 0 && wq == 0 && j == 0 && w == 0) ZG_TR(k, 1);
+        if (lane == 0 && wq == 0 && w == 0) ZG_T2(k, j, 2);
       }
       // ---- item epilogue: row sum from both halves; each half writes its O columns
       lx[w * BQ + r] = ell;

@@ -147,16 +147,13 @@ __device__ __forceinline__ float group_max(uint32_t* sr, int vc) {
 template <int W>
 __device__ __forceinline__ void group_emit(const uint32_t* sr, uint32_t pa, float c, float mc, float& rs) {
   uint32_t pk[W / 2];
-  float r0 = 0.f, r1 = 0.f;
+  const unsigned long long c2 = f32x2(c, c), m2 = f32x2(-mc, -mc);
+  unsigned long long acc = f32x2(0.f, 0.f);
 #pragma unroll
-  for (int j = 0; j < W / 2; ++j) {
-    float a, b;
-    ex2x2(fmaf(__uint_as_float(sr[2 * j]), c, -mc), fmaf(__uint_as_float(sr[2 * j + 1]), c, -mc), a, b);
-    r0 += a;
-    r1 += b;
-    pk[j] = pack_bf16(a, b);
-  }
-  rs += r0 + r1;
+  for (int j = 0; j < W / 2; ++j)
+    pk[j] = exp2_pair_bf16(__uint_as_float(sr[2 * j]), __uint_as_float(sr[2 * j + 1]), c2, m2, acc);
+  const float2 r2 = unpack_f32x2(acc);
+  rs += r2.x + r2.y;
   if constexpr (W == 32) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "

@@ -290,6 +290,32 @@ __device__ __forceinline__ void st_global_32B(void* dst, uint4 lo, uint4 hi) {
                "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
                : "memory");
 }
+// softmax numerator of a pair of logits on the packed fp32 pipes: t = s * c + m2 (FFMA2, m2 =
+// (-mc, -mc)), p = 2^t in fp32 (two MUFU.EX2: the f16x2 / bf16x2 ex2 forms also issue one MUFU
+// op per element on sm_100, and round the argument), acc += p (FADD2); returns p as bf16x2
+__device__ __forceinline__ unsigned long long f32x2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 unpack_f32x2(unsigned long long v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ uint32_t exp2_pair_bf16(float s0, float s1, unsigned long long c2, unsigned long long m2,
+                                                   unsigned long long& acc) {
+  unsigned long long t;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(t) : "l"(f32x2(s0, s1)), "l"(c2), "l"(m2));
+  const float2 tt = unpack_f32x2(t);
+  float e0, e1;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(tt.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(tt.y));
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(acc) : "l"(f32x2(e0, e1)));
+  uint32_t p;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(e1), "f"(e0));
+  return p;
+}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
