@@ -73,16 +73,6 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// two exponentials with one MUFU op: 2^a, 2^b through ex2.approx.f16x2.  The arguments are
-// <= ~8 (lazy max), so the fp16 rounding of the argument costs <= 0.14% relative on the terms
-// that matter, below the bf16 rounding of P that follows.
-__device__ __forceinline__ void ex2x2(float a, float b, float& ea, float& eb) {
-  uint32_t h;
-  asm("{\n\t.reg .b32 t;\n\tcvt.rn.f16x2.f32 t, %2, %1;\n\tex2.approx.f16x2 %0, t;\n\t}" : "=r"(h) : "f"(a), "f"(b));
-  __half2 hh = *reinterpret_cast<__half2*>(&h);
-  ea = __low2float(hh);
-  eb = __high2float(hh);
-}
 __device__ __forceinline__ uint4 scale_pack8(const uint32_t* v, float s) {
   uint4 w;
   w.x = pack_bf16(__uint_as_float(v[0]) * s, __uint_as_float(v[1]) * s);
