@@ -210,7 +210,9 @@ class StripeSortEncoder:
                 h = K.layernorm_rows(xs, blk.ln1_g, blk.ln1_b, npr, out=ws["h"][:mx], n_dev=nn)
             with tr.span("gemm_qkv", flops=(nn, 2.0 * C * 3 * C)):
                 qkv = K.gemm(h, blk.qkv_w, blk.qkv_b, out=ws["qkv"][:R], row_map=npr, m_dev=nn)
-                K.fill_flagged_rows(qkv, self._pad_qkv_row(blk), od.maps["l_is_pad"])
+                # K and V columns only: pad tokens are keys / values of the window, but their own
+                # query rows are dropped (o_rows), so their Q part is never needed
+                K.fill_flagged_rows(qkv[:, C:], self._pad_qkv_row(blk)[0, C:], od.maps["l_is_pad"])
             with tr.span(f"attn_{blk.kind}", flops=4.0 * dh * E * U * H,
                          bytes=U * H * 4 * S * dh * 2 + H * 2 * S * w * 4):
                 o = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], units=U, heads=H, sq=S, sk=S, dh=dh,
