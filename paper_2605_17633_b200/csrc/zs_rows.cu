@@ -25,8 +25,13 @@ __global__ void __launch_bounds__(256, MAXV <= 10 ? 3 : 2) ln_rows_kernel(const 
   if (n_dev) nn = min((long long)*n_dev, n);
   const int lane = threadIdx.x & 31;
   const int C4 = C >> 2;
-  for (long long i = (long long)blockIdx.x * 8 + (threadIdx.x >> 5); i < nn; i += (long long)gridDim.x * 8) {
-    const long long src = rows ? (long long)rows[i] : i;
+  const long long step = (long long)gridDim.x * 8;
+  long long i = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  // source row index one row ahead, so a row's data loads never wait on its index load
+  long long src_next = (rows && i < nn) ? (long long)__ldg(rows + i) : i;
+  for (; i < nn; i += step) {
+    const long long src = src_next;
+    if (i + step < nn) src_next = rows ? (long long)__ldg(rows + i + step) : i + step;
     const long long dst = out_rows ? (long long)out_rows[i] : i;
     const float4* xr = reinterpret_cast<const float4*>(x + src * ldx);
     float4 v[MAXV];
