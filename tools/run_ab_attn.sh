@@ -1,3 +1,2 @@
-timeout 400 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_relpos.py -q -x -k "attention or relpos" --timeout 120 2>&1 | tail -3
-timeout 100 python tools/attn_ab.py global 64 2>&1 | tail -7
+timeout 300 python -m pytest tests/test_gpu_kernels.py -q -x -k "attention_local or attention_window or row_map" --timeout 120 2>&1 | tail -2
 timeout 100 python tools/attn_ab.py local 64 rows 2>&1 | tail -7
