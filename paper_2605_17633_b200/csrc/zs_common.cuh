@@ -284,15 +284,6 @@ __device__ __forceinline__ float gelu_erf(float x) {
   const float erf_v = copysignf(erf_abs, x);
   return 0.5f * x * (1.0f + erf_v);
 }
-// 32-byte global store (sm_100 st.global.v8): one full sector per thread; dst 32-byte aligned
-__device__ __forceinline__ void st_global_32B(void* dst, uint4 lo, uint4 hi) {
-  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(lo.x), "r"(lo.y), "r"(lo.z),
-               "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
-               : "memory");
-}
-// softmax numerator of a pair of logits on the packed fp32 pipes: t = s * c + m2 (FFMA2, m2 =
-// (-mc, -mc)), p = 2^t in fp32 (two MUFU.EX2: the f16x2 / bf16x2 ex2 forms also issue one MUFU
-// op per element on sm_100, and round the argument), acc += p (FADD2); returns p as bf16x2
 __device__ __forceinline__ unsigned long long f32x2(float a, float b) {
   unsigned long long r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
@@ -303,6 +294,56 @@ __device__ __forceinline__ float2 unpack_f32x2(unsigned long long v) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
   return r;
 }
+// gelu_erf on a pair with ONE MUFU op per element: erf(z) = 1 - (1 + a1 z + ... + a6 z^6)^-16
+// (Abramowitz-Stegun 7.1.28, |error| <= 3e-7, far below the bf16 rounding of the output), the
+// polynomial and the four squarings on the packed fp32 pipes (FFMA2 / FMUL2)
+__device__ __forceinline__ void gelu_erf_x2(float& x0, float& x1) {
+  auto k2 = [](float v) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(r) : "f"(v));
+    return r;
+  };
+  auto fma2 = [](unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+  };
+  auto mul2 = [](unsigned long long a, unsigned long long b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+  };
+  const unsigned long long z = mul2(k2(0.7071067811865476f), f32x2(fabsf(x0), fabsf(x1)));
+  unsigned long long p = fma2(k2(0.0000430638f), z, k2(0.0002765672f));
+  p = fma2(p, z, k2(0.0001520143f));
+  p = fma2(p, z, k2(0.0092705272f));
+  p = fma2(p, z, k2(0.0422820123f));
+  p = fma2(p, z, k2(0.0705230784f));
+  p = fma2(p, z, k2(1.0f));
+  p = mul2(p, p);
+  p = mul2(p, p);
+  p = mul2(p, p);
+  p = mul2(p, p);  // ^16 (inf for large z: rcp -> 0, erf -> 1)
+  const float2 q = unpack_f32x2(p);
+  float r0, r1;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r0) : "f"(q.x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(q.y));
+  // 0.5 x (1 + sign(x) (1 - r)) = hx + hx * sign(x) (1 - r)
+  const float e0 = copysignf(1.0f - r0, x0), e1 = copysignf(1.0f - r1, x1);
+  const unsigned long long hx = mul2(k2(0.5f), f32x2(x0, x1));
+  const float2 y = unpack_f32x2(fma2(hx, f32x2(e0, e1), hx));
+  x0 = y.x;
+  x1 = y.y;
+}
+// 32-byte global store (sm_100 st.global.v8): one full sector per thread; dst 32-byte aligned
+__device__ __forceinline__ void st_global_32B(void* dst, uint4 lo, uint4 hi) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(lo.x), "r"(lo.y), "r"(lo.z),
+               "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
+               : "memory");
+}
+// softmax numerator of a pair of logits on the packed fp32 pipes: t = s * c + m2 (FFMA2, m2 =
+// (-mc, -mc)), p = 2^t in fp32 (two MUFU.EX2: the f16x2 / bf16x2 ex2 forms also issue one MUFU
+// op per element on sm_100, and round the argument), acc += p (FADD2); returns p as bf16x2
 __device__ __forceinline__ uint32_t exp2_pair_bf16(float s0, float s1, unsigned long long c2, unsigned long long m2,
                                                    unsigned long long& acc) {
   unsigned long long t;

@@ -39,6 +39,9 @@ def call(lib, kind):
     if kind == "proj16":  # same shape, bf16 output (no fp32 residual traffic)
         lib.zs_gemm_bf16(0, P(a), C, P(wp), C, M, C, C, None, P(out), C, None, 0, None, None, 0, None, st)
         return 2.0 * M * C * C
+    if kind == "fc1nogelu":  # fc1 shape, plain bias epilogue
+        lib.zs_gemm_bf16(0, P(a), C, P(w1), C, Mk, 4 * C, C, None, P(hid), 4 * C, None, 0, None, None, 0, None, st)
+        return 2.0 * Mk * 4 * C * C
     if kind == "fc1":
         lib.zs_gemm_bf16(1, P(a), C, P(w1), C, Mk, 4 * C, C, None, P(hid), 4 * C, None, 0, None, None, 0, None, st)
         return 2.0 * Mk * 4 * C * C
@@ -47,16 +50,37 @@ def call(lib, kind):
 
 
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-for rnd in range(3):
-    for kind in (sys.argv[2].split(",") if len(sys.argv) > 2 else ("qkv", "proj", "proj16", "fc1", "fc2")):
-        for name, lib in libs.items():
-            for _ in range(2):
-                call(lib, kind)
-            torch.cuda.synchronize()
-            e0.record()
-            for _ in range(10):
-                fl = call(lib, kind)
-            e1.record()
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / 10
-            print(f"round {rnd} {kind:5s} {name}: {ms:7.3f} ms {fl / ms / 1e9:7.1f} TF/s", flush=True)
+kinds = sys.argv[2].split(",") if len(sys.argv) > 2 else ("qkv", "proj", "proj16", "fc1", "fc2")
+PAIRS = 24  # paired, finely interleaved samples: the power-capped clock drifts between rounds
+
+
+def batch(lib, kind, n=5):
+    e0.record()
+    for _ in range(n):
+        fl = call(lib, kind)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / n, fl
+
+
+for kind in kinds:
+    for lib in libs.values():
+        for _ in range(3):
+            call(lib, kind)
+    torch.cuda.synchronize()
+    ratios, tn, to = [], [], []
+    for i in range(PAIRS):
+        order = ("new", "old") if i % 2 == 0 else ("old", "new")
+        t = {}
+        for name in order:
+            t[name], fl = batch(libs[name], kind)
+        ratios.append(t["new"] / t["old"])
+        tn.append(t["new"])
+        to.append(t["old"])
+    ratios.sort()
+    tn.sort()
+    to.sort()
+    med = ratios[len(ratios) // 2]
+    print(f"{kind:9s} new/old median {med:.4f} (q1 {ratios[len(ratios) // 4]:.4f} q3 {ratios[3 * len(ratios) // 4]:.4f})"
+          f"  new {tn[len(tn) // 2]:.3f} ms  old {to[len(to) // 2]:.3f} ms  new {fl / tn[len(tn) // 2] / 1e9:.0f} TF/s",
+          flush=True)
