@@ -367,3 +367,38 @@ class SparseSAMImageEncoder:
         x0 = self.embed(img)
         xo = self.core.forward_rows(x0.view(B, g.h, g.w, self.cfg.d), mode, out=self._bufs(B)["xo"])
         return self.neck(xo, B, out=out)
+
+
+class GraphedImageEncoder:
+    """CUDA-graph replay of a :class:`SparseSAMImageEncoder` forward for a fixed batch size.
+
+    The whole forward (patch embed, orderings, every block's ~9 launches, neck) has no host
+    synchronisation (device-side row counts, grow-only scratch), so it is captured once into a
+    CUDA graph over static input / output buffers and replayed: one graph launch instead of
+    ~300 kernel launches from Python per call, which is what bounds small batches (one image).
+    """
+
+    def __init__(self, enc: SparseSAMImageEncoder, batch: int, mode: str = "sparse"):
+        g = enc.cfg.grid
+        dev = enc.device
+        self.enc, self.batch, self.mode = enc, batch, mode
+        self.img = torch.zeros((batch, 3, g.h * SAM_PATCH, g.w * SAM_PATCH), device=dev, dtype=torch.float32)
+        self.out = torch.empty((batch, g.h, g.w, SAM_NECK), device=dev, dtype=torch.float32)
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):  # warm-up: scratch / workspaces allocated outside the capture
+            for _ in range(2):
+                enc(self.img, mode, out=self.out)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            enc(self.img, mode, out=self.out)
+
+    def __call__(self, img: torch.Tensor) -> torch.Tensor:
+        """[batch, 3, H, W] fp32 -> the static output buffer [batch, 64, 64, 256] (valid until the
+        next call)."""
+        if tuple(img.shape) != tuple(self.img.shape):
+            raise ValueError(f"graph captured for images of shape {tuple(self.img.shape)}, got {tuple(img.shape)}")
+        self.img.copy_(img, non_blocking=True)
+        self.graph.replay()
+        return self.out

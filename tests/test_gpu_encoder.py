@@ -130,3 +130,20 @@ def test_sam_frame_vs_fp32_torch_twin():
                                     padding=1)
     n2 = torch.nn.functional.layer_norm(n2.permute(0, 2, 3, 1), (256,), frame.neck_ln2_g, frame.neck_ln2_b, 1e-6)
     assert float((out - n2).norm() / n2.norm()) < 1e-2
+
+
+def test_cuda_graph_replay_matches_eager():
+    """The whole image-encoder forward captured into one CUDA graph (no host syncs inside) replays
+    bit-identically to the eager call, for new inputs copied into the static buffer."""
+    from paper_2605_17633_b200.encoder import GraphedImageEncoder
+
+    cfg = Z.sam_config("vit_b", 0.4)
+    enc = SparseSAMImageEncoder(cfg, random_params(cfg, "cuda", seed=5), random_frame(cfg, "cuda", seed=6))
+    gr = GraphedImageEncoder(enc, 2)
+    for seed in (0, 1):
+        img = torch.randn(2, 3, 1024, 1024, device="cuda", generator=torch.Generator(device="cuda").manual_seed(seed))
+        got = gr(img).clone()
+        ref = enc(img)
+        assert torch.equal(got, ref)
+    with pytest.raises(ValueError):
+        gr(torch.zeros(1, 3, 1024, 1024, device="cuda"))
