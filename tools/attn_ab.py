@@ -60,16 +60,33 @@ def call(lib, out):
 
 
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-for rnd in range(3):
-    for name, lib in libs.items():
-        for _ in range(2):
-            call(lib, outs[name])
-        torch.cuda.synchronize()
-        e0.record()
-        for _ in range(10):
-            call(lib, outs[name])
-        e1.record()
-        torch.cuda.synchronize()
-        print(f"round {rnd} {kind} {name}: {e0.elapsed_time(e1) / 10:7.3f} ms", flush=True)
+PAIRS = 20  # paired, finely interleaved samples: the power-capped clock drifts between rounds
+
+
+def batch(name, n=4):
+    e0.record()
+    for _ in range(n):
+        call(libs[name], outs[name])
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / n
+
+
+for name in libs:
+    for _ in range(2):
+        call(libs[name], outs[name])
+torch.cuda.synchronize()
+ratios, tn, to = [], [], []
+for i in range(PAIRS):
+    order = ("new", "old") if i % 2 == 0 else ("old", "new")
+    t = {name: batch(name) for name in order}
+    ratios.append(t["new"] / t["old"])
+    tn.append(t["new"])
+    to.append(t["old"])
+for v in (ratios, tn, to):
+    v.sort()
+m = PAIRS // 2
+print(f"{kind} new/old median {ratios[m]:.4f} (q1 {ratios[PAIRS // 4]:.4f} q3 {ratios[3 * PAIRS // 4]:.4f})  "
+      f"new {tn[m]:.3f} ms  old {to[m]:.3f} ms", flush=True)
 d = (outs["new"].float() - outs["old"].float()).norm() / outs["old"].float().norm()
 print("rel diff new vs old:", d.item())
