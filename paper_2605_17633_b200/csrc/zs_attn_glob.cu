@@ -40,7 +40,7 @@ constexpr int OST = 2;  // one-hot ring stages (generated on chip: no memory lat
 constexpr int QST = 1;  // Q slots (the next item's Q loads once the last S' of the item completed)
 constexpr int VST = 3;  // V ring stages
 constexpr uint32_t TM_S = 0;     // S_w at [w*128, w*128+128)
-constexpr uint32_t TM_O = 256;   // O_w at 256 + w*80
+constexpr uint32_t TM_O = 256;   // O at [256, 256 + DH), row sums (ones MMA) at [256 + DH, +16)
 constexpr uint32_t TM_BQ = 416;  // Bq: 128 fp16 = 64 columns
 constexpr int OH_BYTES = 2 * BQ * 128;  // two 64-column SW128 slabs (e_ky | e_kx)
 
@@ -54,7 +54,7 @@ struct Params {
   const int* k_sp;
   float tau;
   __nv_bfloat16* out;
-  int off_q, off_k, off_oh, off_v, off_ml, off_bar, tile;
+  int off_q, off_k, off_oh, off_v, off_ml, off_ones, off_bar, tile;
   int trace;
 };
 
@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       const uint64_t dk = sdesc_k_sw128(smem + P.off_k), dkt = sdesc_k_sw32(smem + P.off_k + L::MAIN);
       const uint64_t doh = sdesc_k_sw128(smem + P.off_oh);
       const uint64_t dv = sdesc_mn_sw128(smem + P.off_v), dvt = sdesc_mn_sw32(smem + P.off_v + L::MAIN);
+      const uint64_t dones = sdesc_mn_sw32(smem + P.off_ones);
       // S'(c) of chunk ordinal c into S_w: q.k (bf16) then + Bq . OH^T (fp16, A from TMEM)
       int first_c = 0;  // chunk ordinal of the current item's first chunk (trace only)
       auto issue_s = [&](int c, int k, int w, bool last) {
@@ -287,6 +288,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
           const uint32_t acc = (!first || ks > 0) ? 1u : 0u;
           umma_ts(d, a0 + 8 * ks, v + ks * (16 * 128 / 16), id_pv, acc);
           if constexpr (kTail) umma_ts(d + 64, a0 + 8 * ks, vt + ks * (16 * 32 / 16), id_pv2, acc);
+          umma_ts(d + DH, a0 + 8 * ks, dones + ks * (16 * 32 / 16), id_pv2, acc);  // row sums of P
         }
         umma_commit_elect(o_full);
         umma_commit_elect(&v_empty[vs]);
@@ -340,6 +342,13 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       const uint32_t one = 0x3C00u;  // fp16 1.0
       const int kbase = (warp - 2) * 64;
       const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+      {  // bf16 ones [128, 16] (every element 1.0, so the swizzle is irrelevant); published to the
+         // tensor core by the fence before the first oh_full arrive
+        const uint4 o4 = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          reinterpret_cast<uint4*>(smem + P.off_ones)[((warp - 2) * 32 + lane) * 4 + q] = o4;
+      }
 #pragma unroll
       for (int st = 0; st < OST; ++st)
 #pragma unroll
@@ -431,7 +440,6 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     const uint32_t o_addr = tmem + TM_O + lane_off;
     const uint32_t bq_addr = tmem + TM_BQ + w * 32 + lane_off;  // this half's 64 fp16 bias columns
     float* xch = reinterpret_cast<float*>(smem + P.off_ml);     // [chunk parity][half][BQ] partial max
-    float* lx = xch + 4 * BQ;                                   // [half][BQ] partial row sums
     const uint32_t pair_bar = 1 + wq;
     constexpr float L2E = 1.4426950408889634f;
     constexpr float kThr = 5.545177444479562f;  // ln 256
@@ -482,28 +490,51 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(bq_full);
     };
-    // O columns of this half: [40w, 40w + 32) and [40w + 32, 40w + 40) (dh = 80), or
-    // [32w, 32w + 32) (dh = 64)
+    // O columns this half rescales: half 0 [0, OH), half 1 [OH, DH + 16) incl. the row-sum columns
+    // [DH, DH + 16) of the ones MMA; OH = DH / 2 (40 or 32)
     constexpr int OH = DH / 2;
-    auto o_scale = [&](float alpha) {
+    auto ld_x8 = [&](uint32_t a, uint32_t (&r)[8]) {
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                   : "r"(a));
+    };
+    auto st_x8 = [&](uint32_t a, const uint32_t (&r)[8]) {
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(a), "r"(r[0]),
+                   "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                   : "memory");
+    };
+    auto scale32 = [&](uint32_t a, float alpha) {
       uint32_t pr[32];
-      tmem_ld32(o_addr + w * OH, pr);
+      tmem_ld32(a, pr);
       tmem_ld_wait();
 #pragma unroll
       for (int q = 0; q < 32; ++q) pr[q] = __float_as_uint(__uint_as_float(pr[q]) * alpha);
-      tmem_st32(o_addr + w * OH, pr);
-      if constexpr (OH == 40) {
-        uint32_t p8[8];
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(p8[0]), "=r"(p8[1]), "=r"(p8[2]), "=r"(p8[3]), "=r"(p8[4]), "=r"(p8[5]),
-                       "=r"(p8[6]), "=r"(p8[7])
-                     : "r"(o_addr + w * OH + 32));
-        tmem_ld_wait();
+      tmem_st32(a, pr);
+    };
+    auto scale16 = [&](uint32_t a, float alpha) {
+      uint32_t pr[16];
+      tmem_ld16(a, pr);
+      tmem_ld_wait();
 #pragma unroll
-        for (int q = 0; q < 8; ++q) p8[q] = __float_as_uint(__uint_as_float(p8[q]) * alpha);
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(o_addr + w * OH + 32),
-                     "r"(p8[0]), "r"(p8[1]), "r"(p8[2]), "r"(p8[3]), "r"(p8[4]), "r"(p8[5]), "r"(p8[6]), "r"(p8[7])
-                     : "memory");
+      for (int q = 0; q < 16; ++q) pr[q] = __float_as_uint(__uint_as_float(pr[q]) * alpha);
+      tmem_st16(a, pr);
+    };
+    auto scale8 = [&](uint32_t a, float alpha) {
+      uint32_t pr[8];
+      ld_x8(a, pr);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) pr[q] = __float_as_uint(__uint_as_float(pr[q]) * alpha);
+      st_x8(a, pr);
+    };
+    auto o_scale = [&](float alpha) {
+      if (w == 0) {
+        scale32(o_addr, alpha);
+        if constexpr (OH == 40) scale8(o_addr + 32, alpha);
+      } else {
+        scale32(o_addr + OH, alpha);
+        scale16(o_addr + OH + 32, alpha);
+        if constexpr (OH == 40) scale8(o_addr + OH + 48, alpha);
       }
     };
 
@@ -519,7 +550,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       const int nc = n_chunks(P, i);
       const int row = i * BQ + r;
       if (lane == 0 && wq == 0) ZG_TR(k, 2 + w);
-      float m_ref = -INFINITY, ell = 0.f;
+      float m_ref = -INFINITY;
       for (int j = 0; j < nc; ++j, ++c) {
         const int buf = c & 1;
         const int cj = chunk_of(P, i, j);
@@ -567,18 +598,15 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         }
         const float mc = (m_ref == -INFINITY) ? 0.f : m_ref * L2E;
         const unsigned long long c2 = f32x2(cexp, cexp), m2 = f32x2(-mc, -mc);
-        unsigned long long acc = f32x2(0.f, 0.f);
 #pragma unroll
         for (int g = 0; g < 2; ++g) {
           uint32_t pk[16];
 #pragma unroll
           for (int q = 0; q < 16; ++q)
-            pk[q] = exp2_pair_bf16(__uint_as_float(sr[32 * g + 2 * q]), __uint_as_float(sr[32 * g + 2 * q + 1]), c2,
-                                   m2, acc);
+            pk[q] = exp2_pair_bf16_ns(__uint_as_float(sr[32 * g + 2 * q]), __uint_as_float(sr[32 * g + 2 * q + 1]),
+                                      c2, m2);
           tmem_st16(s_addr + 32 * w + 16 * g, pk);  // P (bf16) of keys [64w + 32g, +32)
         }
-        const float2 rs = unpack_f32x2(acc);
-        ell = ell * alpha + (rs.x + rs.y);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -586,15 +614,19 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         if (lane == 0 && wq == 0 && j == 0 && w == 0) ZG_TR(k, 1);
         if (lane == 0 && wq == 0 && w == 0) ZG_T2(k, j, 2);
       }
-      // ---- item epilogue: row sum from both halves; each half writes its O columns
-      lx[w * BQ + r] = ell;
+      // ---- item epilogue: the row sum is O column DH (ones MMA); each half writes its O columns
       // the item's last PV(c - 1).  o_full completes once per chunk; parity waits are exact only
       // one phase ahead, and s_full(c - 1) guaranteed PV(c - 3) only: wait PV(c - 2) first
       mbar_wait(o_full, (c - 2) & 1);
       mbar_wait(o_full, (c - 1) & 1);
-      named_bar_sync(pair_bar, 64);
       tc_fence_after();
-      const float inv = 1.0f / (ell + lx[(w ^ 1) * BQ + r]);
+      float inv;
+      {
+        uint32_t l1;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(l1) : "r"(o_addr + DH));
+        tmem_ld_wait();
+        inv = 1.0f / __uint_as_float(l1);
+      }
       bool valid = row < P.S;
       long long orow_off = (long long)u * P.o_unit_stride + (long long)row * P.ldo;
       if (valid && P.o_rows) {
@@ -691,6 +723,7 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
   p.off_oh = take(OST * OH_BYTES, 1024);
   p.off_v = take(VST * tile, 1024);
   p.off_ml = take(2 * 4 * BQ * 4, 16);
+  p.off_ones = take(BQ * 32, 1024);  // [128 keys, 16] bf16 ones: B operand of the row-sum MMA
   p.off_bar = take(256, 8);
   const size_t smem = 1024 + (size_t)off;
   if (smem > 227 * 1024) return 1;

@@ -357,6 +357,19 @@ __device__ __forceinline__ uint32_t exp2_pair_bf16(float s0, float s1, unsigned 
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(e1), "f"(e0));
   return p;
 }
+// exp2_pair_bf16 without the row sum (the PV MMA accumulates it through a ones column)
+__device__ __forceinline__ uint32_t exp2_pair_bf16_ns(float s0, float s1, unsigned long long c2,
+                                                      unsigned long long m2) {
+  unsigned long long t;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(t) : "l"(f32x2(s0, s1)), "l"(c2), "l"(m2));
+  const float2 tt = unpack_f32x2(t);
+  float e0, e1;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(tt.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(tt.y));
+  uint32_t p;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(e1), "f"(e0));
+  return p;
+}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
