@@ -162,7 +162,9 @@ ZS_API int zs_gemm_bf16(int epi, const void* A, long long lda, const void* W, lo
  *   tiles b_row x b_col, active key tiles J_i = {0..prefix-1} ∪ {min(i, Tc-1)}
  *   logits = tau*q·k + bh[q_sp, k_sp / w] + bw[q_sp, k_sp % w]
  *   out [units][Sq][ldo] bf16, head h at columns h*dh
- * dh must be 64 or 80.  Unit strides are in elements.
+ * dh must be 64 or 80.  Unit strides are in elements.  The fp16 bias operands the tensor-core
+ * kernels read are built per call into a library-owned grow-only scratch per (device, stream)
+ * (allocated on the first call of a larger shape; calls on different streams never share it).
  * replaces: attention.py:167-221 `ashape_attention` (and :88-104 `build_active_set`). */
 ZS_API int zs_stripe_attn_fwd(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                        long long q_unit_stride, long long kv_unit_stride, int units, int heads, int sq, int sk,

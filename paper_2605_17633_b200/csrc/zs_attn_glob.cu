@@ -727,29 +727,19 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
   p.off_bar = take(256, 8);
   const size_t smem = 1024 + (size_t)off;
   if (smem > 227 * 1024) return 1;
-  // fp16 bias operand rows [heads, S, 128] (scratch, grow-only per device); per-unit fp32
+  // fp16 bias operand rows [heads, S, 128] (library scratch per device and stream); per-unit fp32
   // tables (contiguous: bias_us == heads * S * w) -> [units, heads, S, 128]; or the caller's
   if (bias_us && !btab_ext && bias_us != (long long)heads * S * bias_w) return 1;
   if (btab_ext) {
     p.btab = btab_ext;
     p.btab_us = btab_us;
   } else {
-    static __half* buf[64] = {nullptr};
-    static size_t cap[64] = {0};
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return ZS_ERR_DEVICE;
     const size_t need = (size_t)heads * S * 128 * (bias_us ? units : 1);
-    if (cap[dev] < need) {
-      if (buf[dev]) cudaFree(buf[dev]);
-      buf[dev] = nullptr;
-      cap[dev] = 0;
-      if (cudaMalloc(&buf[dev], need * sizeof(__half)) != cudaSuccess) return ZS_ERR_DEVICE;
-      cap[dev] = need;
-    }
+    __half* buf = reinterpret_cast<__half*>(scratch(kScratchGlobBias, need * sizeof(__half), st));
+    if (!buf) return ZS_ERR_DEVICE;
     const long long n = (long long)need;
-    glob_bias_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(bh, bw, n / 128, bias_w, 1.0f / tau,
-                                                                        buf[dev]);
-    p.btab = buf[dev];
+    glob_bias_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(bh, bw, n / 128, bias_w, 1.0f / tau, buf);
+    p.btab = buf;
     p.btab_us = bias_us ? (long long)heads * S * 128 : 0;
   }
   CUtensorMap m[6];

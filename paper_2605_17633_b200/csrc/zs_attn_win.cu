@@ -589,22 +589,6 @@ using namespace zs;
 
 static inline int ceil16(int x) { return (x + 15) & ~15; }
 
-// fp16 bias-operand table scratch (per device, grow-only; allocated on first use of a size)
-static __half* win_btab(size_t elems) {
-  static __half* buf[64] = {nullptr};
-  static size_t cap[64] = {0};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  if (cap[dev] < elems) {
-    if (buf[dev]) cudaFree(buf[dev]);
-    buf[dev] = nullptr;
-    cap[dev] = 0;
-    if (cudaMalloc(&buf[dev], elems * sizeof(__half)) != cudaSuccess) return nullptr;
-    cap[dev] = elems;
-  }
-  return buf[dev];
-}
-
 // Host launcher.  Returns 1 when the shape / schedule is outside this kernel's envelope
 // (the caller then uses the generic window kernel), 0 on launch, negative on error.
 int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
@@ -741,7 +725,7 @@ int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, 
   // followed by the [S, 32] one-hot key rows
   if (bias_us && !btab_ext && bias_us != (long long)heads * S * bias_w) return 1;
   const long long trows = btab_ext ? 0 : (long long)heads * S * (bias_us ? units : 1);
-  __half* btab = win_btab((size_t)(trows + S) * 32);
+  __half* btab = reinterpret_cast<__half*>(scratch(kScratchWinBias, (size_t)(trows + S) * 32 * sizeof(__half), st));
   if (!btab) return ZS_ERR_DEVICE;
   {
     const long long n = (trows + S) * 32;

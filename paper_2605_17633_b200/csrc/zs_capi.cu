@@ -3,12 +3,35 @@
 // fc1+GELU -> fc2+scatter-add residual).
 #include <cudaTypedefs.h>
 
+#include <map>
 #include <mutex>
+#include <tuple>
 
 #include "zs_common.cuh"
 #include "zs_host.h"
 
 namespace zs {
+
+// Library-owned scratch (e.g. the attention kernels' fp16 bias-operand tables): one grow-only
+// buffer per (device, stream, slot), so calls on different streams never share it; guarded by a
+// mutex (the entry points are reentrant).  Growing frees the old buffer (cudaFree synchronises
+// the device, after which no kernel can still read it); steady-state calls allocate nothing.
+void* scratch(int slot, size_t bytes, cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, cudaStream_t, int>, std::pair<void*, size_t>> bufs;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& e = bufs[std::make_tuple(dev, st, slot)];
+  if (e.second < bytes) {
+    if (e.first) cudaFree(e.first);
+    e.first = nullptr;
+    e.second = 0;
+    if (cudaMalloc(&e.first, bytes) != cudaSuccess) return nullptr;
+    e.second = bytes;
+  }
+  return e.first;
+}
 
 
 

@@ -384,15 +384,18 @@ class GraphedImageEncoder:
         self.enc, self.batch, self.mode = enc, batch, mode
         self.img = torch.zeros((batch, 3, g.h * SAM_PATCH, g.w * SAM_PATCH), device=dev, dtype=torch.float32)
         self.out = torch.empty((batch, g.h, g.w, SAM_NECK), device=dev, dtype=torch.float32)
+        # warm-up and capture on the same side stream: the library's scratch is per (device,
+        # stream), so everything the captured launches use is allocated before the capture
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream(dev))
-        with torch.cuda.stream(side):  # warm-up: scratch / workspaces allocated outside the capture
+        with torch.cuda.stream(side):
             for _ in range(2):
                 enc(self.img, mode, out=self.out)
-        torch.cuda.current_stream(dev).wait_stream(side)
+        side.synchronize()
         self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
+        with torch.cuda.graph(self.graph, stream=side):
             enc(self.img, mode, out=self.out)
+        torch.cuda.current_stream(dev).wait_stream(side)
 
     def __call__(self, img: torch.Tensor) -> torch.Tensor:
         """[batch, 3, H, W] fp32 -> the static output buffer [batch, 64, 64, 256] (valid until the

@@ -1,2 +1,1 @@
 timeout 900 python -m pytest tests -q -x -m gpu --timeout 200 2>&1 | tail -2
-timeout 600 python bench.py --no-cpu --no-dense > gpurun_out/bench_q.log 2>&1; tail -1 gpurun_out/bench_q.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'], d['clocks']['sm_mhz']); [print(' ', k, round(v['ms_per_step'],2)) for k,v in d['kernels'].items()]"
