@@ -379,3 +379,30 @@ def test_attention_output_row_map_and_pad_helpers():
     K.fill_flagged_rows(dst, src, flag)
     assert torch.equal(dst[flag.bool()], src.expand(4, 24))
     assert bool((dst[~flag.bool()] == 0).all())
+
+
+@pytest.mark.parametrize("S,w,tile", [(196, 14, 32), (4096, 64, 128)])
+def test_attention_concurrent_streams(S, w, tile):
+    """Two streams run the attention at once with different bias tables: the library's bias-
+    operand scratch is per (device, stream), so each result equals its own sequential run."""
+    g = torch.Generator().manual_seed(21)
+    units, heads, dh = (40 if S <= 256 else 2), 2, 80
+    C = heads * dh
+    qkv = torch.randn(units * S, 3 * C, generator=g).bfloat16().to(DEV)
+    sp = torch.stack([torch.randperm(S, generator=g) for _ in range(units)]).int().to(DEV)
+    tabs = [((0.5 * torch.randn(heads, S, w, generator=g)).to(DEV), (0.5 * torch.randn(heads, S, w, generator=g)).to(DEV))
+            for _ in range(2)]
+    kw = dict(units=units, heads=heads, sq=S, sk=S, dh=dh, q_sp=sp, k_sp=sp, b_row=tile, b_col=tile, prefix=2,
+              tau=dh ** -0.5)
+    ref = [K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], bh=bh, bw=bw, **kw) for bh, bw in tabs]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    outs = [torch.empty_like(r) for r in ref]
+    for _ in range(3):
+        for s_, (bh, bw), o in zip(streams, tabs, outs):
+            s_.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s_):
+                K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], bh=bh, bw=bw, out=o, **kw)
+        torch.cuda.synchronize()
+        for o, r in zip(outs, ref):
+            assert torch.equal(o, r)

@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests -q -x -m gpu --timeout 200 2>&1 | tail -2
+timeout 300 python -m pytest tests/test_gpu_kernels.py -q -x -k "concurrent" --timeout 200 2>&1 | tail -2
