@@ -17,3 +17,4 @@ ls -la gpurun_out
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"zs_gemm2|zs_attn_win|zs_attn_glob" -s 3 -c 6 \
     -o gpurun_out/bench_full -f python bench.py --profile --steps 1 --warmup 1 > /dev/null 2>&1; echo "ncu bench_full rc=$?"
 ls -la gpurun_out
+timeout 900 python tools/density_sweep.py 16 --out gpurun_out/density_sweep.json > gpurun_out/density_sweep.log 2>&1; echo "sweep rc=$?"
