@@ -301,6 +301,34 @@ __global__ void patchify_kernel(const float* __restrict__ img, int B, int Cin, i
     out[e] = __float2bfloat16_rn(img[(((long long)b * Cin + c) * H + y) * W + x]);
   }
 }
+// Vectorised patchify for P % 8 == 0 (SAM: P = 16): one thread moves one P-pixel image row
+// segment of one patch (P floats in, P bf16 out, contiguous on both sides).  Consecutive
+// threads take consecutive patches along x, so a warp reads 32 adjacent segments of one image
+// row (coalesced) and writes whole 16-byte chunks of 32 patch rows.
+template <int P>
+__global__ void patchify_vec_kernel(const float* __restrict__ img, int B, int Cin, int H, int W,
+                                    __nv_bfloat16* __restrict__ out) {
+  const int gw = W / P, gh = H / P;
+  const long long total = (long long)B * Cin * H * gw;
+  const int ncol = Cin * P * P;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int tx = (int)(e % gw);
+    const long long r1 = e / gw;  // (b * Cin + c) * H + y
+    const int y = (int)(r1 % H);
+    const long long bc = r1 / H;
+    const int c = (int)(bc % Cin), b = (int)(bc / Cin);
+    const float4* src = reinterpret_cast<const float4*>(img + r1 * W + (long long)tx * P);
+    const long long row = ((long long)b * gh + y / P) * gw + tx;
+    uint4* dst = reinterpret_cast<uint4*>(out + row * ncol + c * P * P + (y % P) * P);
+#pragma unroll
+    for (int q = 0; q < P / 8; ++q) {
+      const float4 a = __ldg(src + 2 * q), d = __ldg(src + 2 * q + 1);
+      dst[q] = make_uint4(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w), pack_bf16(d.x, d.y), pack_bf16(d.z, d.w));
+    }
+  }
+}
+
 // 3x3 / stride 1 / pad 1 im2col of channels-last bf16 rows, TAP-MAJOR columns:
 // out[row, (ky*3 + kx)*C + c] = x[b, y+ky-1, x+kx-1, c] (zeros outside).  One thread moves 8
 // channels (16 bytes): reads and writes are contiguous runs of C channels.
@@ -439,8 +467,12 @@ extern "C" int zs_prefix_keep_rows(int U, int S_, int K, const uint8_t* is_pad, 
 extern "C" int zs_patchify(const float* img, int B, int Cin, int H, int W, int P, void* out, zs_stream_t stream) {
   if (B <= 0) return 0;
   if (!img || !out || P <= 0 || H % P || W % P) return ZS_ERR_SHAPE;
-  patchify_kernel<<<num_sms() * 8, 256, 0, S(stream)>>>(img, B, Cin, H, W, P,
-                                                         reinterpret_cast<__nv_bfloat16*>(out));
+  if (P == 16 && (reinterpret_cast<uintptr_t>(img) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0)
+    patchify_vec_kernel<16><<<num_sms() * 8, 256, 0, S(stream)>>>(img, B, Cin, H, W,
+                                                                 reinterpret_cast<__nv_bfloat16*>(out));
+  else
+    patchify_kernel<<<num_sms() * 8, 256, 0, S(stream)>>>(img, B, Cin, H, W, P,
+                                                           reinterpret_cast<__nv_bfloat16*>(out));
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }
 

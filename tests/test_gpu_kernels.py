@@ -406,3 +406,14 @@ def test_attention_concurrent_streams(S, w, tile):
         torch.cuda.synchronize()
         for o, r in zip(outs, ref):
             assert torch.equal(o, r)
+
+
+@pytest.mark.parametrize("B,H,W,P", [(2, 1024, 1024, 16), (1, 64, 96, 16), (2, 48, 40, 8)])
+def test_patchify_bit_exact(B, H, W, P):
+    """Patch extraction of the SAM patch embed (16x16/16 conv as GEMM rows): bf16 of the same
+    pixels in (c, ky, kx) column order, vectorised kernel (P = 16) and generic kernel."""
+    img = torch.randn(B, 3, H, W, device=DEV)
+    got = K.patchify(img, P)
+    ref = (img.view(B, 3, H // P, P, W // P, P).permute(0, 2, 4, 1, 3, 5)
+           .reshape(B * (H // P) * (W // P), 3 * P * P).bfloat16())
+    assert torch.equal(got, ref)
