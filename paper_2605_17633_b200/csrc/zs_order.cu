@@ -47,22 +47,38 @@ __global__ void __launch_bounds__(256) sobel_kernel(const float* __restrict__ x,
       in_w[a][c] = grid_ok && (ny / win == py / win) && (nx / win == px / win) && ny >= 0 && nx >= 0;
     }
 
+  // halo staging, software-pipelined: the 16-byte loads of pass c0 + CC are in flight (in
+  // registers) while pass c0 is computed from shared memory
+  constexpr int NLD = (HY * HX * (CC / 4) + 255) / 256;
+  const bool vec = (C & 3) == 0 && (C % CC) == 0;
+  float4 pre[NLD];
+  auto load_pass = [&](int c0) {
+#pragma unroll
+    for (int k = 0; k < NLD; ++k) {
+      const int e = threadIdx.x + 256 * k;
+      pre[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e < HY * HX * (CC / 4)) {
+        const int q = e % (CC / 4), pp = e / (CC / 4);
+        const int gy = y0 + pp / HX - 1, gx = x0 + pp % HX - 1;
+        if (gy >= 0 && gx >= 0 && gy < H && gx < W)
+          pre[k] = __ldg(reinterpret_cast<const float4*>(xb + ((long long)gy * W + gx) * C + c0) + q);
+      }
+    }
+  };
+  if (vec) load_pass(0);
   for (int c0 = 0; c0 < C; c0 += CC) {
     __syncthreads();
-    if ((C & 3) == 0 && c0 + CC <= C) {  // 16-byte loads: 4 channels per thread
-      for (int e = threadIdx.x; e < HY * HX * (CC / 4); e += 256) {
-        const int q = e % (CC / 4);
-        const int p = e / (CC / 4);
-        const int hy = p / HX, hx = p % HX;
-        const int gy = y0 + hy - 1, gx = x0 + hx - 1;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (gy >= 0 && gx >= 0 && gy < H && gx < W)
-          v = __ldg(reinterpret_cast<const float4*>(xb + ((long long)gy * W + gx) * C + c0) + q);
-        float* t = tile + p * CCP + 4 * q;
-        t[0] = v.x;
-        t[1] = v.y;
-        t[2] = v.z;
-        t[3] = v.w;
+    if (vec) {
+#pragma unroll
+      for (int k = 0; k < NLD; ++k) {
+        const int e = threadIdx.x + 256 * k;
+        if (e < HY * HX * (CC / 4)) {
+          float* t = tile + (e / (CC / 4)) * CCP + 4 * (e % (CC / 4));
+          t[0] = pre[k].x;
+          t[1] = pre[k].y;
+          t[2] = pre[k].z;
+          t[3] = pre[k].w;
+        }
       }
     } else {
       for (int e = threadIdx.x; e < HY * HX * CC; e += 256) {
@@ -76,6 +92,7 @@ __global__ void __launch_bounds__(256) sobel_kernel(const float* __restrict__ x,
       }
     }
     __syncthreads();
+    if (vec && c0 + CC < C) load_pass(c0 + CC);
     const int cn = min(CC, C - c0);
     for (int ch = 0; ch < cn; ++ch) {
       float v[3][3];
