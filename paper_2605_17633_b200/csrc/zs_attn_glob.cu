@@ -151,6 +151,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
   uint64_t* s_full = bar + 24;   // [wg]
   uint64_t* p_full = bar + 26;   // [S buffer]  8 softmax warps: P of the chunk in TMEM
   uint64_t* o_full = bar + 28;   // PV of a chunk completed (one completion per chunk)
+  uint64_t* o_last = bar + 29;   // the item's last PV completed (one completion per item)
   uint64_t* o_free = bar + 30;   // 8 warps: O_0 / O_1 read by the item's epilogue
   uint64_t* bq_full = bar + 31;  // 8 warps: the item's Bq rows are in TMEM
   uint64_t* bq_free = bar + 32;  // the item's last S' completed (Bq may be replaced)
@@ -172,8 +173,9 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
       mbar_init(&p_full[s], 8);
-      mbar_init(&o_full[s], 1);
     }
+    mbar_init(o_full, 1);
+    mbar_init(o_last, 1);
     for (int s = 0; s < KST; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -330,6 +332,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         // the item's last PV now: its epilogue (and with it the next item's Bq install, which
         // the next S' waits for) depends on it
         flush_pv();
+        umma_commit_elect(o_last);  // after the item's last PV: the epilogue's own barrier
         pend_c = -1;
       }
     } else {
@@ -612,13 +615,13 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[buf]);
         if (lane == 0 && wq == 0 && j == 0 && w == 0) ZG_TR(k, 1);
+
         if (lane == 0 && wq == 0 && w == 0) ZG_T2(k, j, 2);
       }
       // ---- item epilogue: the row sum is O column DH (ones MMA); each half writes its O columns
-      // the item's last PV(c - 1).  o_full completes once per chunk; parity waits are exact only
-      // one phase ahead, and s_full(c - 1) guaranteed PV(c - 3) only: wait PV(c - 2) first
-      mbar_wait(o_full, (c - 2) & 1);
-      mbar_wait(o_full, (c - 1) & 1);
+      // the item's last PV: its own barrier (one completion per item), not an o_full parity,
+      // which could already have moved past it by the time this warp waits
+      mbar_wait(o_last, k & 1);
       tc_fence_after();
       float inv;
       {
@@ -670,6 +673,8 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         load_bq(it + 2 * G, sp_nn, bqx);
         sp_nn = load_sp(it + 3 * G);
       }
+      // next item's bias rows into TMEM once this item's last S' has completed
+
     }
   }
   tc_fence_before();
@@ -724,7 +729,7 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
   p.off_v = take(VST * tile, 1024);
   p.off_ml = take(2 * 4 * BQ * 4, 16);
   p.off_ones = take(BQ * 32, 1024);  // [128 keys, 16] bf16 ones: B operand of the row-sum MMA
-  p.off_bar = take(256, 8);
+  p.off_bar = take(512, 8);
   const size_t smem = 1024 + (size_t)off;
   if (smem > 227 * 1024) return 1;
   // fp16 bias operand rows [heads, S, 128] (library scratch per device and stream); per-unit fp32
