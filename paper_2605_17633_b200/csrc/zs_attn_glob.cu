@@ -615,7 +615,6 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[buf]);
         if (lane == 0 && wq == 0 && j == 0 && w == 0) ZG_TR(k, 1);
-
         if (lane == 0 && wq == 0 && w == 0) ZG_T2(k, j, 2);
       }
       // ---- item epilogue: the row sum is O column DH (ones MMA); each half writes its O columns
@@ -673,8 +672,6 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         load_bq(it + 2 * G, sp_nn, bqx);
         sp_nn = load_sp(it + 3 * G);
       }
-      // next item's bias rows into TMEM once this item's last S' has completed
-
     }
   }
   tc_fence_before();
