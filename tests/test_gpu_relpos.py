@@ -147,7 +147,8 @@ def test_relpos_argument_errors():
 
 
 def _twin_blocks(x, params, cfg):
-    """fp32 torch twin of SAM blocks with decomposed rel-pos (windows without pads), r = keep = 1."""
+    """fp32 torch twin of the blocks with SAM decomposed rel-pos, reference pad semantics
+    (zero pads before LN1, MLP on padded windows, crop), r = keep = 1."""
     import torch.nn.functional as F
 
     from paper_2605_17633_b200.dense import sam_rel_pos_bias
@@ -155,9 +156,11 @@ def _twin_blocks(x, params, cfg):
     B, Hh, Ww, C = x.shape
     H, win = cfg.heads, cfg.window
     dh = C // H
+    Hp, Wp = -(-Hh // win) * win, -(-Ww // win) * win
     for p in params:
-        if p.kind == "local":
-            t = x.view(B, Hh // win, win, Ww // win, win, C).permute(0, 1, 3, 2, 4, 5).reshape(-1, win * win, C)
+        if p.kind == "local":  # zero pads re-created every local block (encoder.py:356), then windows
+            xp = F.pad(x, (0, 0, 0, Wp - Ww, 0, Hp - Hh))
+            t = xp.view(B, Hp // win, win, Wp // win, win, C).permute(0, 1, 3, 2, 4, 5).reshape(-1, win * win, C)
         else:
             t = x.reshape(B, Hh * Ww, C)
         N, S, _ = t.shape
@@ -169,25 +172,30 @@ def _twin_blocks(x, params, cfg):
         t = t + o @ p.proj_w.float().T + p.proj_b
         hh = F.layer_norm(t, (C,), p.ln2_g, p.ln2_b, 1e-6)
         t = t + F.gelu(hh @ p.w1.float().T + p.b1) @ p.w2.float().T + p.b2
-        if p.kind == "local":
-            x = t.view(B, Hh // win, Ww // win, win, win, C).permute(0, 1, 3, 2, 4, 5).reshape(B, Hh, Ww, C)
+        if p.kind == "local":  # merge windows and crop the pads (encoder.py:366-368)
+            x = t.view(B, Hp // win, Wp // win, win, win, C).permute(0, 1, 3, 2, 4, 5).reshape(B, Hp, Wp, C)
+            x = x[:, :Hh, :Ww].contiguous()
         else:
             x = t.view(B, Hh, Ww, C)
     return x
 
 
-def test_encoder_rel_pos_mode_vs_fp32_twin():
+@pytest.mark.parametrize("side", [28, 30])
+def test_encoder_rel_pos_mode_vs_fp32_twin(side):
     """Whole local + global blocks in SAM rel-pos mode at r = keep = 1 vs the fp32 torch twin
-    (tolerance of tests/test_gpu_encoder.py: cos >= 0.999, rel. Frobenius <= 3e-2)."""
+    (tolerance of tests/test_gpu_encoder.py: cos >= 0.999, rel. Frobenius <= 3e-2); side 30
+    pads the windows (30 -> 42), exercising the pad-token path (constant K/V rows, dropped
+    query rows) with q-dependent biases."""
     import paper_2605_17633_b200 as Z
     from paper_2605_17633_b200.encoder import StripeSortEncoder
     from paper_2605_17633_b200.weights import random_params
 
-    cfg = Z.EncoderConfig(grid=Z.GridShape(28, 28), d=320, heads=4, window=14, layout=("local", "global", "local"),
-                          r=1.0, keep_fraction=1.0)
+    cfg = Z.EncoderConfig(grid=Z.GridShape(side, side), d=320, heads=4, window=14,
+                          layout=("local", "global", "local"), r=1.0, keep_fraction=1.0)
     params = random_params(cfg, DEV, seed=4, rel_pos=True, rel_pos_std=0.5)
-    assert params[0].bh is None and params[0].rel_pos_h.shape == (27, 80) and params[1].rel_pos_h.shape == (55, 80)
-    x = torch.randn(2, 28, 28, 320, device=DEV)
+    assert params[0].bh is None and params[0].rel_pos_h.shape == (27, 80)
+    assert params[1].rel_pos_h.shape == (2 * side - 1, 80)
+    x = torch.randn(2, side, side, 320, device=DEV)
     got = StripeSortEncoder(cfg, params)(x).double()
     ref = _twin_blocks(x, params, cfg).double()
     cos = float((got * ref).sum() / (got.norm() * ref.norm()))

@@ -1,3 +1,1 @@
-timeout 900 python -m pytest tests -q -x -m gpu --timeout 200 2>&1 | tail -2
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 600 python bench.py > gpurun_out/bench_final.log 2>&1; tail -1 gpurun_out/bench_final.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'], d['dense_baseline']['value'], d['roofline']['frac'], d['cpu_baseline']['value'], d['clocks'])"
+timeout 300 python -m pytest tests/test_gpu_relpos.py -q -x -k encoder --timeout 200 2>&1 | tail -4
