@@ -354,12 +354,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
           for (int i = 0; i < 8; ++i) xa[i] = xb[i];
         }
       } else {
-#pragma unroll 1
-        for (int c = 0; c < BN / 2; c += 32) {
-          uint32_t r[32];
-          __syncwarp();
-          tmem_ld32(trow + c, r);
-          tmem_ld_wait();
+        // TMEM loads software-pipelined: chunk c + 1 is in flight while chunk c is converted
+        // and stored (tcgen05.wait::ld then covers both)
+        static_assert(BN / 2 == 128, "four 32-column chunks per warp");
+        uint32_t ra[32], rb[32];
+        __syncwarp();
+        tmem_ld32(trow, ra);
+        tmem_ld_wait();
+        auto emit = [&](const uint32_t (&r)[32], int c) {
           const int nb = n0 + chalf * (BN / 2) + c;
           if (valid && nb < N) {
             float v[32];
@@ -376,24 +378,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
                 v[4 * j + 3] += b.w;
               }
             }
-            if constexpr (EPI == 0 || EPI == 1) {
-              if constexpr (EPI == 1) {
+            if constexpr (EPI == 1) {
 #pragma unroll
-                for (int j = 0; j < 16; ++j) gelu_erf_x2(v[2 * j], v[2 * j + 1]);
-              }
-              uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(ep.out) + orow * ep.ld_out + nb);
+              for (int j = 0; j < 16; ++j) gelu_erf_x2(v[2 * j], v[2 * j + 1]);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(ep.out) + orow * ep.ld_out + nb);
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                uint4 w;
-                w.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
-                w.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
-                w.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
-                w.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
-                dst[j] = w;
-              }
+            for (int j = 0; j < 4; ++j) {
+              uint4 w;
+              w.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
+              w.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
+              w.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
+              w.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
+              dst[j] = w;
             }
           }
-        }
+        };
+        tmem_ld32(trow + 32, rb);
+        emit(ra, 0);
+        tmem_ld_wait();
+        tmem_ld32(trow + 64, ra);
+        emit(rb, 32);
+        tmem_ld_wait();
+        tmem_ld32(trow + 96, rb);
+        emit(ra, 64);
+        tmem_ld_wait();
+        emit(rb, 96);
       }
       __syncwarp();
       tc_fence_before();
