@@ -1,3 +1,2 @@
-timeout 900 python -m pytest tests -q -x -m gpu --timeout 200 2>&1 | tail -2
+timeout 900 python -m pytest tests -q -x -m gpu --timeout 200 > gpurun_out/pytest_gpu.log 2>&1; tail -2 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 600 python bench.py --no-cpu --no-dense > gpurun_out/bench_q.log 2>&1; tail -1 gpurun_out/bench_q.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'], d['roofline']['frac'], d['clocks']['sm_mhz'])"
