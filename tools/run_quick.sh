@@ -1,2 +1,3 @@
-timeout 600 python bench.py > gpurun_out/bench_final.log 2>&1; tail -1 gpurun_out/bench_final.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'], d['dense_baseline']['value'], d['roofline']['frac'], d['cpu_baseline']['value'], d['gpu_launches'], d['clocks'], d['config']['l2'])"
-timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log | cut -c1-200
+for b in 8 64; do
+timeout 600 python bench.py --batch $b --no-cpu --no-dense --steps 10 --warmup 5 2>/tmp/err.log | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$b', round(d['value'],1), round(d['e2e']['value'],1), d['config']['cuda_graph'], d['gpu_launches'], d['clocks']['sm_mhz'])" || tail -5 /tmp/err.log
+done
