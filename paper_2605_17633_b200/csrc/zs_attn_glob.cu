@@ -11,16 +11,19 @@
 //    [bh[σq(r)] | bw[σq(r)]] / tau (fp16, 128 columns, resident in TMEM for the item and used
 //    as the A operand) and OH[k] = [e_{σk/64} | e_{σk%64}] (fp16 one-hot rows of the chunk's
 //    keys, generated in shared memory).  logit = tau * S', so the softmax does no gathers.
-//  * Two softmax warpgroups split the chunks (WG w takes the CTA's chunk ordinals c with
-//    c % 2 == w, so S(c) always targets the other WG's S buffer than S(c-1)), each with its
-//    own S buffer, O accumulator and running max / sum; the partial results merge once per
-//    item (each WG writes half of the output columns).
-//  * P (bf16) overwrites the WG's S columns in TMEM and is the A operand of the PV MMA.
-//  * Lazy rescaling: O_w is rescaled in TMEM only when the row max grows by more than ln 256.
-//  * The next item's Bq rows are loaded from the fp16 table and written into TMEM
-//    (tcgen05.st) by the softmax threads once the item's last S' MMA has completed.
+//  * Chunk c's S' goes to TMEM S buffer c % 2, so S'(c + 1) is computed while chunk c is in
+//    the softmax.  All 8 softmax warps work on every chunk: the two warps of a TMEM lane
+//    quarter (warps 4 + q and 8 + q) split its 128 keys (64 each) and exchange partial row
+//    maxima through shared memory (one 64-thread named barrier per chunk).
+//  * P (bf16) overwrites the chunk's S columns in TMEM and is the A operand of the PV MMA.  One
+//    O accumulator per CTA; the PV MMA also multiplies P by a ones matrix into 16 extra O
+//    columns, which hold the row sums (of the bf16 P exactly as applied to V).
+//  * Lazy rescaling: O (and its row-sum columns) is rescaled in TMEM, warp-wide, only when a
+//    row max grows by more than ln 256.
+//  * The next item's Bq rows are prefetched from the fp16 table one item ahead and written into
+//    TMEM (tcgen05.st) by the softmax threads once the item's last S' MMA has completed.
 // Roles: warp 0 TMA (lane 0: Q per item + K per chunk, lane 1: V per chunk), warp 1 MMA (whole
-// warp, elected lane), warps 2-3 one-hot key rows per chunk, warps 4-7 WG0, warps 8-11 WG1.
+// warp, elected lane), warps 2-3 one-hot key rows per chunk, warps 4-11 softmax.
 #include <cuda_fp16.h>
 
 #include <algorithm>
