@@ -23,9 +23,10 @@
 //    Q_B rows, which only produce discarded output rows.
 //  * MMA issue order ping-pongs the two softmax warpgroups:
 //      S_A(k) PV_B(k-1) S_B(k) PV_A(k) S_A(k+1) ...
-// Roles: warp 0 TMA, warp 1 MMA, warp 2 TMEM owner, warp 3 bias operands (cp.async gather of
-// the fp16 bias rows by σq, one-hot key rows from σk), warps 4-7 softmax tile A, warps 8-11
-// softmax tile B (one thread per row).
+// Roles: warp 0 TMA, warp 1 MMA, warps 2-3 bias operands by 16-byte cp.async (warp 3: fp16 bias
+// rows by σq, warp 2: one-hot key rows by σk; warp 2 also owns the TMEM allocation), warps 4-7
+// softmax tile A, warps 8-11 softmax tile B (one thread per row; exponentials on the packed fp32
+// pipes, exp2_pair_bf16 in zs_common.cuh).
 #include <cuda_fp16.h>
 
 #include <algorithm>
