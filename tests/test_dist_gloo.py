@@ -65,3 +65,32 @@ def test_sharded_batch_gathers_single_process_result(n_images):
     ref = _per_image(batch).numpy()
     for r in range(world):
         assert np.array_equal(res[r], ref)
+
+
+def _bench_line(*args, timeout=300):
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, str(root / "bench.py"), *args], capture_output=True, text=True,
+                       timeout=timeout, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+@pytest.mark.parametrize("world,batch", [(2, 64), (3, 10)])
+def test_bench_gpus_n_forms_world_and_gathers(world, batch):
+    """`bench.py --gpus N` without WORLD_SIZE re-launches itself as N ranks (torch.distributed.run);
+    the dry run's JSON line reports the world it formed, and the post-run all_gather puts every
+    rank's shard back in its slot (checked bit for bit on every rank)."""
+    line = _bench_line("--gpus", str(world), "--dry-run", "--steps", "2", "--warmup", "1", "--batch", str(batch))
+    assert line["n_gpus"] == world
+    assert line["dry_run"] is True
+    assert line["gather"]["slot_check"] is True
+    assert line["gather"]["bytes_gathered_per_rank"] == batch * 4 * 4 * 3 * 4  # [4, 4, 3] fp32 stand-in per image
+    assert line["config"]["per_rank_batch"] == -(-batch // world)
