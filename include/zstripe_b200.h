@@ -8,8 +8,12 @@
  * Conventions (all entry points):
  *   - returns ZS_OK (0) or a negative zs_status; never throws, never aborts;
  *   - asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream);
- *   - every buffer is caller-allocated device memory; no allocation on the hot path;
- *   - reentrant: no mutable global state besides a lazily-resolved driver symbol;
+ *   - every buffer is caller-allocated device memory, workspaces included (sized by the
+ *     matching *_ws_bytes query, 256-byte aligned); the library never allocates;
+ *   - reentrant: no mutable global state besides a lazily-resolved driver symbol and the
+ *     cached SM count; a workspace must not be shared by calls that may run concurrently;
+ *   - graph-capturable: no entry point synchronises or allocates, so calls may be recorded
+ *     into a CUDA graph (the captured graph keeps the caller's pointers);
  *   - bf16 buffers are `void*` (IEEE bfloat16, little endian), indices are int32.
  * Only sm_100a (B200) is supported; there is no CPU fallback.
  */
@@ -38,13 +42,17 @@ enum zs_status {
   ZS_ERR_ALIGN = -3,       /* pointer / leading dimension misaligned         */
   ZS_ERR_LAUNCH = -4,      /* CUDA launch failure (see cudaGetLastError)     */
   ZS_ERR_TMAP = -5,        /* cuTensorMapEncodeTiled rejected the operand    */
-  ZS_ERR_DEVICE = -6       /* no sm_100 device / driver symbol unavailable   */
+  ZS_ERR_DEVICE = -6,      /* no sm_100 device / driver symbol unavailable   */
+  ZS_ERR_WORKSPACE = -7    /* workspace NULL or below the *_ws_bytes query   */
 };
 
 /* Human-readable text for a zs_status value. */
 ZS_API const char* zs_status_string(int status);
-/* ABI version (major*100 + minor). */
+/* ABI version (major*100 + minor).  2.00: caller-owned attention workspaces (ws, ws_bytes). */
 ZS_API int zs_abi_version(void);
+/* Kernels this library has launched from the calling thread so far (a per-thread counter; the
+ * host reads it around calls to count exactly what a composite entry point launched). */
+ZS_API unsigned long long zs_launch_counter(void);
 
 /* ------------------------------------------------------------------ ordering
  * Sobel gradient-magnitude saliency of an fp32 token grid x[B, H, W, C]
@@ -162,15 +170,16 @@ ZS_API int zs_gemm_bf16(int epi, const void* A, long long lda, const void* W, lo
  *   tiles b_row x b_col, active key tiles J_i = {0..prefix-1} ∪ {min(i, Tc-1)}
  *   logits = tau*q·k + bh[q_sp, k_sp / w] + bw[q_sp, k_sp % w]
  *   out [units][Sq][ldo] bf16, head h at columns h*dh
- * dh must be 64 or 80.  Unit strides are in elements.  The fp16 bias operands the tensor-core
- * kernels read are built per call into a library-owned grow-only scratch per (device, stream)
- * (allocated on the first call of a larger shape; calls on different streams never share it).
+ * dh must be 64 or 80.  Unit strides are in elements.  ws: caller-owned device workspace of at
+ * least zs_stripe_attn_ws_bytes(units, heads, sq, sk, dh, 0) bytes, 256-byte aligned; the fp16
+ * bias operand rows the tensor-core kernels read are built into it per call.
  * replaces: attention.py:167-221 `ashape_attention` (and :88-104 `build_active_set`). */
+ZS_API size_t zs_stripe_attn_ws_bytes(int units, int heads, int sq, int sk, int dh, int per_unit_bias);
 ZS_API int zs_stripe_attn_fwd(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                        long long q_unit_stride, long long kv_unit_stride, int units, int heads, int sq, int sk,
                        int dh, const float* bh, const float* bw, int bias_w, const int32_t* q_sp,
                        const int32_t* k_sp, int b_row, int b_col, int prefix_tiles, float tau, void* out,
-                       long long ldo, long long o_unit_stride, zs_stream_t stream);
+                       long long ldo, long long o_unit_stride, void* ws, size_t ws_bytes, zs_stream_t stream);
 /* Same, with an output row map: row r of unit u goes to out row o_rows[u*sq + r] (head h at
  * columns h*dh), or is not written when o_rows[...] < 0 (o_rows == NULL: the layout above).
  * Lets a caller write only the query rows it keeps (e.g. skip SAM's window pad tokens,
@@ -180,18 +189,19 @@ ZS_API int zs_stripe_attn_fwd_rows(const void* q, const void* k, const void* v, 
                             int sq, int sk, int dh, const float* bh, const float* bw, int bias_w,
                             const int32_t* q_sp, const int32_t* k_sp, int b_row, int b_col, int prefix_tiles,
                             float tau, void* out, long long ldo, long long o_unit_stride, const int32_t* o_rows,
-                            zs_stream_t stream);
+                            void* ws, size_t ws_bytes, zs_stream_t stream);
 
 /* Same as zs_stripe_attn_fwd_rows with one bias table pair PER UNIT: bh / bw of unit u start at
  * u * bias_unit_stride floats (each [heads, S, w], spatial-position rows as above).  The
- * reference's BiasTables (attention.py:28-55) generalised to per-window / per-image tables. */
+ * reference's BiasTables (attention.py:28-55) generalised to per-window / per-image tables.
+ * ws >= zs_stripe_attn_ws_bytes(units, heads, sq, sk, dh, 1) bytes. */
 ZS_API int zs_stripe_attn_fwd_unit_bias(const void* q, const void* k, const void* v, long long ldq, long long ldk,
                                         long long ldv, long long q_unit_stride, long long kv_unit_stride, int units,
                                         int heads, int sq, int sk, int dh, const float* bh, const float* bw,
                                         long long bias_unit_stride, int bias_w, const int32_t* q_sp,
                                         const int32_t* k_sp, int b_row, int b_col, int prefix_tiles, float tau,
                                         void* out, long long ldo, long long o_unit_stride, const int32_t* o_rows,
-                                        zs_stream_t stream);
+                                        void* ws, size_t ws_bytes, zs_stream_t stream);
 
 /* ------------------------------------------------ SAM decomposed relative position (q-dependent)
  * SAM's add_decomposed_rel_pos (not in the reference, whose bias tables are static: SURVEY §8(f)

@@ -35,12 +35,14 @@ SIGNATURES: dict[str, list] = {
     "zs_layernorm_rows": [_p, _ll, _p, _ll, _i, _p, _p, _f, _p, _ll, _i, _p],
     "zs_layernorm_rows_ex": [_p, _ll, _p, _p, _ll, _p, _i, _p, _p, _f, _p, _ll, _i, _p],
     "zs_gemm_bf16": [_i, _p, _ll, _p, _ll, _i, _i, _i, _p, _p, _ll, _p, _ll, _p, _p, _i, _p, _p],
+    "zs_launch_counter": [],  # returns unsigned long long
+    "zs_stripe_attn_ws_bytes": [_i, _i, _i, _i, _i, _i],  # returns size_t
     "zs_stripe_attn_fwd": [_p, _p, _p, _ll, _ll, _ll, _ll, _ll, _i, _i, _i, _i, _i, _p, _p, _i, _p, _p, _i, _i,
-                           _i, _f, _p, _ll, _ll, _p],
+                           _i, _f, _p, _ll, _ll, _p, _sz, _p],
     "zs_stripe_attn_fwd_rows": [_p, _p, _p, _ll, _ll, _ll, _ll, _ll, _i, _i, _i, _i, _i, _p, _p, _i, _p, _p, _i, _i,
-                                _i, _f, _p, _ll, _ll, _p, _p],
+                                _i, _f, _p, _ll, _ll, _p, _p, _sz, _p],
     "zs_stripe_attn_fwd_unit_bias": [_p, _p, _p, _ll, _ll, _ll, _ll, _ll, _i, _i, _i, _i, _i, _p, _p, _ll, _i, _p,
-                                     _p, _i, _i, _i, _f, _p, _ll, _ll, _p, _p],
+                                     _p, _i, _i, _i, _f, _p, _ll, _ll, _p, _p, _sz, _p],
     "zs_relpos_ws_bytes": [_i, _i, _i, _i, _i],  # returns size_t
     "zs_relpos_bias": [_p, _ll, _ll, _i, _i, _i, _i, _i, _p, _p, _p, _p, _p, _p, _sz, _p],
     "zs_stripe_attn_fwd_relpos": [_p, _p, _p, _ll, _ll, _ll, _ll, _ll, _i, _i, _i, _i, _p, _p, _i, _p, _p, _i, _i, _i,
@@ -52,6 +54,7 @@ SIGNATURES: dict[str, list] = {
     "zs_im2col3x3": [_p, _i, _i, _i, _i, _p, _p],
 }
 
+ABI_VERSION = 200
 _lib: C.CDLL | None = None
 
 
@@ -73,6 +76,10 @@ def load() -> C.CDLL:
         fn.argtypes = args
         fn.restype = _i
     lib.zs_relpos_ws_bytes.restype = _sz
+    lib.zs_stripe_attn_ws_bytes.restype = _sz
+    lib.zs_launch_counter.restype = C.c_ulonglong
+    if lib.zs_abi_version() != ABI_VERSION:
+        raise RuntimeError(f"{LIB_PATH} has ABI {lib.zs_abi_version()}, expected {ABI_VERSION}: rebuild it")
     _lib = lib
     return lib
 
@@ -85,16 +92,17 @@ def status_string(rc: int) -> str:
     return load().zs_status_string(rc).decode()
 
 
-# kernel launches issued per successful ABI call (composites launch several)
-LAUNCHES_PER_CALL = {"zs_rc_mlp_fwd": 3, "zs_unit_span_rows": 3, "zs_prefix_keep_rows": 3, "zs_layout_maps": 3,
-                     "zs_abi_version": 0, "zs_relpos_ws_bytes": 0, "zs_relpos_bias": 2,
-                     "zs_stripe_attn_fwd_relpos": 4}
+# kernels launched through the library, counted by the library itself (zs_launch_counter: every
+# <<<>>> site in csrc/ increments a per-thread counter), so composites and optional prep kernels
+# are counted exactly
 launch_count = 0
 
 
 def call(name: str, *args) -> None:
     global launch_count
-    rc = getattr(load(), name)(*args)
+    lib = load()
+    n0 = lib.zs_launch_counter()
+    rc = getattr(lib, name)(*args)
+    launch_count += lib.zs_launch_counter() - n0
     if rc != 0:
         raise RuntimeError(f"{name} failed: zs_status {rc} ({status_string(rc)})")
-    launch_count += LAUNCHES_PER_CALL.get(name, 1)

@@ -21,7 +21,6 @@ permutations, active sets and keep-sets are bit-exact.
 from __future__ import annotations
 
 import math
-import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -425,7 +424,14 @@ def encoder_forward(x, weights, cfg: EncoderConfig, mode: str = "sparse"):
     """Run every block over [H, W, D] (or a batch [B, H, W, D]); returns (output, CostReport).
 
     ``weights`` are reference-layout block weights (``BlockWeights`` / oracle
-    blocks) or already-converted ``BlockParams``.
+    blocks) or already-converted ``BlockParams``.  ``CostReport.ms`` holds each
+    block's device time (CUDA events around its launches).
+
+    Shape envelope of the B200 block engine: head dim d / heads must be 64 or 80
+    and d a multiple of 64 (the SAM ViT-B/L/H widths); other widths, e.g. the
+    reference's toy default d = 64 with 4 heads (dh = 16), raise ValueError.  The
+    per-op entry points (``ashape_attention``, ``route_mlp``) zero-pad heads up to
+    80 and take any width.
     """
     if mode not in ("dense", "sparse"):
         raise ValueError(f"mode must be 'dense' or 'sparse', got {mode!r}")
@@ -441,10 +447,13 @@ def encoder_forward(x, weights, cfg: EncoderConfig, mode: str = "sparse"):
     xt = _to_dev(x)
     if single:
         xt = xt[None]
-    t0 = time.perf_counter()
+    # per-block device time from CUDA events around each block's launches (the reference's
+    # per-block wall clock, encoder.py:342,372; the first block also carries the layout switch
+    # out of the spatial order, the orderings and final permute are outside every block)
+    enc.block_events = []
     y = enc(xt, mode)
     torch.cuda.synchronize()
-    ms = (time.perf_counter() - t0) * 1e3
-    per = [ms / len(cfg.layout)] * len(cfg.layout)
+    per = [s.elapsed_time(e) for s, e in enc.block_events]
+    enc.block_events = None
     y = y[0] if single else y
     return _like(y, x), cost_report(cfg, mode, per)

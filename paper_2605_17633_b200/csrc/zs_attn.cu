@@ -689,12 +689,12 @@ int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, 
                     long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
                     const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
                     float tau, void* out, long long ldo, long long ous, const int* o_rows, long long bias_us,
-                    const __half* btab_ext, long long btab_us, cudaStream_t st);
+                    const __half* btab_ext, long long btab_us, void* ws, size_t ws_bytes, cudaStream_t st);
 int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                      long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
                      const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
                      float tau, void* out, long long ldo, long long ous, const int* o_rows, long long bias_us,
-                     const __half* btab_ext, long long btab_us, cudaStream_t st);
+                     const __half* btab_ext, long long btab_us, void* ws, size_t ws_bytes, cudaStream_t st);
 int launch_attn_local(const void* q, const void* k, const void* v, long long ldq, long long ldk, long long ldv,
                       long long qus, long long kvus, int units, int heads, int sq, int sk, int dh, const float* bh,
                       const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col,
@@ -727,7 +727,7 @@ static int launch_attn(const CUtensorMap* m, attn::Params p, cudaStream_t st) {
   cudaFuncSetAttribute(zs_attn_kernel<DH, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int grid = num_sms();
   if (grid > p.items) grid = p.items;
-  zs_attn_kernel<DH, FAST><<<grid, attn::kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p);
+  { zs_attn_kernel<DH, FAST><<<grid, attn::kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p); count_launch(); }
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }
 
@@ -787,7 +787,7 @@ static int attn_dispatch(const void* q, const void* k, const void* v, long long 
                          int dh, const float* bh, const float* bw, long long bias_us, int bias_w, const int32_t* q_sp,
                          const int32_t* k_sp, int b_row, int b_col, int prefix_tiles, float tau, void* out,
                          long long ldo, long long o_unit_stride, const int32_t* o_rows, const __half* btab_ext,
-                         long long btab_us, cudaStream_t st) {
+                         long long btab_us, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (units <= 0 || heads <= 0) return 0;
   if (!q || !k || !v || ((!bh || !bw) && !btab_ext) || !q_sp || !k_sp || !out) return ZS_ERR_ARG;
   if (sq <= 0 || sk <= 0 || b_row <= 0 || b_col <= 0 || bias_w <= 0 || bias_w > 255) return ZS_ERR_SHAPE;
@@ -808,7 +808,7 @@ static int attn_dispatch(const void* q, const void* k, const void* v, long long 
     if (sq == sk && !getenv("ZS_ATTN_NO_WIN")) {
       const int rc = launch_attn_win(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, dh, bh,
                                      bw, bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride,
-                                     o_rows, bias_us, btab_ext, btab_us, st);
+                                     o_rows, bias_us, btab_ext, btab_us, ws, ws_bytes, st);
       if (rc <= 0 || btab_ext) return rc;
     }
     if (btab_ext) return 1;
@@ -819,7 +819,7 @@ static int attn_dispatch(const void* q, const void* k, const void* v, long long 
   if (sq == sk && !getenv("ZS_ATTN_NO_GLOB")) {  // 128x128 tiles: split-chunk TMEM-P kernel (zs_attn_glob.cu)
     const int rc = launch_attn_glob(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, dh, bh, bw,
                                     bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride, o_rows,
-                                    bias_us, btab_ext, btab_us, st);
+                                    bias_us, btab_ext, btab_us, ws, ws_bytes, st);
     if (rc <= 0 || btab_ext) return rc;
   }
   if (btab_ext) return 1;
@@ -852,15 +852,31 @@ static int attn_dispatch(const void* q, const void* k, const void* v, long long 
   return launch_attn_dh<80>(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, p, st);
 }
 
+// fp16 bias-operand rows the window / global kernels read (built per call from the fp32 tables
+// into the caller's workspace): window [tables * heads * S + S, 32] halves (the trailing S rows are
+// the one-hot key rows), global [tables * heads * S, 128] halves; tables = units for per-unit
+// bias, else 1.  The generic kernels need none.
+static size_t attn_ws_bytes(int units, int heads, int sq, int sk, int per_unit) {
+  if (units <= 0 || heads <= 0 || sq <= 0 || sk <= 0) return 0;
+  const size_t tables = per_unit ? (size_t)units : 1;
+  const size_t halves = (sq <= 256 && sk <= 256) ? (tables * heads * sq + sq) * 32 : tables * heads * sq * 128;
+  return (halves * sizeof(__half) + 255) & ~(size_t)255;
+}
+
+extern "C" size_t zs_stripe_attn_ws_bytes(int units, int heads, int sq, int sk, int dh, int per_unit_bias) {
+  if (dh != 64 && dh != 80) return 0;
+  return attn_ws_bytes(units, heads, sq, sk, per_unit_bias);
+}
+
 extern "C" int zs_stripe_attn_fwd(const void* q, const void* k, const void* v, long long ldq, long long ldk,
                                   long long ldv, long long q_unit_stride, long long kv_unit_stride, int units,
                                   int heads, int sq, int sk, int dh, const float* bh, const float* bw, int bias_w,
                                   const int32_t* q_sp, const int32_t* k_sp, int b_row, int b_col,
                                   int prefix_tiles, float tau, void* out, long long ldo, long long o_unit_stride,
-                                  zs_stream_t stream) {
+                                  void* ws, size_t ws_bytes, zs_stream_t stream) {
   return attn_dispatch(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, sk, dh, bh, bw, 0,
                        bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride, nullptr, nullptr,
-                       0, reinterpret_cast<cudaStream_t>(stream));
+                       0, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int zs_stripe_attn_fwd_rows(const void* q, const void* k, const void* v, long long ldq, long long ldk,
@@ -868,10 +884,11 @@ extern "C" int zs_stripe_attn_fwd_rows(const void* q, const void* k, const void*
                                        int heads, int sq, int sk, int dh, const float* bh, const float* bw,
                                        int bias_w, const int32_t* q_sp, const int32_t* k_sp, int b_row, int b_col,
                                        int prefix_tiles, float tau, void* out, long long ldo,
-                                       long long o_unit_stride, const int32_t* o_rows, zs_stream_t stream) {
+                                       long long o_unit_stride, const int32_t* o_rows, void* ws, size_t ws_bytes,
+                                       zs_stream_t stream) {
   return attn_dispatch(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, sk, dh, bh, bw, 0,
                        bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride, o_rows, nullptr,
-                       0, reinterpret_cast<cudaStream_t>(stream));
+                       0, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
 extern "C" int zs_stripe_attn_fwd_unit_bias(const void* q, const void* k, const void* v, long long ldq, long long ldk,
@@ -880,10 +897,11 @@ extern "C" int zs_stripe_attn_fwd_unit_bias(const void* q, const void* k, const 
                                             const float* bw, long long bias_unit_stride, int bias_w,
                                             const int32_t* q_sp, const int32_t* k_sp, int b_row, int b_col,
                                             int prefix_tiles, float tau, void* out, long long ldo,
-                                            long long o_unit_stride, const int32_t* o_rows, zs_stream_t stream) {
+                                            long long o_unit_stride, const int32_t* o_rows, void* ws,
+                                            size_t ws_bytes, zs_stream_t stream) {
   return attn_dispatch(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, sq, sk, dh, bh, bw,
                        bias_unit_stride, bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride,
-                       o_rows, nullptr, 0, reinterpret_cast<cudaStream_t>(stream));
+                       o_rows, nullptr, 0, ws, ws_bytes, reinterpret_cast<cudaStream_t>(stream));
 }
 
 // ---------------------------------------------------------------- SAM relative-position mode
@@ -896,7 +914,9 @@ static size_t relpos_tables_bytes(int units, int heads, int S, int bias_w) {
 
 extern "C" size_t zs_relpos_ws_bytes(int units, int heads, int S, int dh, int bias_w) {
   if (units <= 0 || heads <= 0 || bias_w <= 0 || bias_w > 64 || (dh != 64 && dh != 80)) return 0;
-  return relpos_r_bytes(dh, bias_w) + relpos_tables_bytes(units, heads, S, bias_w);
+  // [R scratch | fp16 operand rows or fp32 tables | the attention's operand workspace (fp32-table path)]
+  return relpos_r_bytes(dh, bias_w) + relpos_tables_bytes(units, heads, S, bias_w) +
+         attn_ws_bytes(units, heads, S, S, 1);
 }
 
 extern "C" int zs_relpos_bias(const void* q, long long ldq, long long q_unit_stride, int units, int heads, int S,
@@ -942,7 +962,7 @@ extern "C" int zs_stripe_attn_fwd_relpos(const void* q, const void* k, const voi
     if (rc == 0) {
       rc = attn_dispatch(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, S, S, dh, nullptr,
                          nullptr, 0, bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride,
-                         o_rows, btab, us, st);
+                         o_rows, btab, us, nullptr, 0, st);
       if (rc <= 0) return rc;
     }
   }
@@ -954,5 +974,6 @@ extern "C" int zs_stripe_attn_fwd_relpos(const void* q, const void* k, const voi
   if (rc) return rc;
   return attn_dispatch(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, S, S, dh, bh, bw,
                        (long long)heads * S * bias_w, bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo,
-                       o_unit_stride, o_rows, nullptr, 0, st);
+                       o_unit_stride, o_rows, nullptr, 0,
+                       tables + relpos_tables_bytes(units, heads, S, bias_w), attn_ws_bytes(units, heads, S, S, 1), st);
 }

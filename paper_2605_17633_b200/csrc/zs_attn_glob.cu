@@ -693,7 +693,7 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
                      long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
                      const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
                      float tau, void* out, long long ldo, long long ous, const int* o_rows, long long bias_us,
-                     const __half* btab_ext, long long btab_us, cudaStream_t st) {
+                     const __half* btab_ext, long long btab_us, void* ws, size_t ws_bytes, cudaStream_t st) {
   using namespace attng;
   if (b_row != BQ || b_col != BQ || (dh != 64 && dh != 80) || S < 1 || bias_w > 64 || !(tau > 0.f)) return 1;
   Params p{};
@@ -732,7 +732,7 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
   p.off_bar = take(512, 8);
   const size_t smem = 1024 + (size_t)off;
   if (smem > 227 * 1024) return 1;
-  // fp16 bias operand rows [heads, S, 128] (library scratch per device and stream); per-unit fp32
+  // fp16 bias operand rows [heads, S, 128] (caller's workspace); per-unit fp32
   // tables (contiguous: bias_us == heads * S * w) -> [units, heads, S, 128]; or the caller's
   if (bias_us && !btab_ext && bias_us != (long long)heads * S * bias_w) return 1;
   if (btab_ext) {
@@ -740,10 +740,11 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
     p.btab_us = btab_us;
   } else {
     const size_t need = (size_t)heads * S * 128 * (bias_us ? units : 1);
-    __half* buf = reinterpret_cast<__half*>(scratch(kScratchGlobBias, need * sizeof(__half), st));
-    if (!buf) return ZS_ERR_DEVICE;
+    if (!ws || ws_bytes < need * sizeof(__half)) return ZS_ERR_WORKSPACE;  // zs_stripe_attn_ws_bytes
+    if (reinterpret_cast<uintptr_t>(ws) & 255) return ZS_ERR_ALIGN;
+    __half* buf = reinterpret_cast<__half*>(ws);
     const long long n = (long long)need;
-    glob_bias_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(bh, bw, n / 128, bias_w, 1.0f / tau, buf);
+    { glob_bias_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(bh, bw, n / 128, bias_w, 1.0f / tau, buf); count_launch(); }
     p.btab = buf;
     p.btab_us = bias_us ? (long long)heads * S * 128 : 0;
   }
@@ -767,10 +768,10 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
   if (grid > p.items) grid = p.items;
   if (dh == 64) {
     cudaFuncSetAttribute(zs_attn_glob_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    zs_attn_glob_kernel<64><<<grid, kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p);
+    { zs_attn_glob_kernel<64><<<grid, kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p); count_launch(); }
   } else {
     cudaFuncSetAttribute(zs_attn_glob_kernel<80>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    zs_attn_glob_kernel<80><<<grid, kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p);
+    { zs_attn_glob_kernel<80><<<grid, kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p); count_launch(); }
   }
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }

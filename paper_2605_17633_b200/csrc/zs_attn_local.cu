@@ -539,12 +539,12 @@ int launch_attn_local(const void* q, const void* k, const void* v, long long ldq
     const size_t smem = attnl::Layout<64>::smem_bytes(bias_w);
     if (smem > 227 * 1024) return ZS_ERR_SHAPE;
     cudaFuncSetAttribute(zs_attn_local_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    zs_attn_local_kernel<64><<<grid, attnl::kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p);
+    { zs_attn_local_kernel<64><<<grid, attnl::kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p); count_launch(); }
   } else {
     const size_t smem = attnl::Layout<80>::smem_bytes(bias_w);
     if (smem > 227 * 1024) return ZS_ERR_SHAPE;
     cudaFuncSetAttribute(zs_attn_local_kernel<80>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    zs_attn_local_kernel<80><<<grid, attnl::kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p);
+    { zs_attn_local_kernel<80><<<grid, attnl::kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p); count_launch(); }
   }
   e = cudaGetLastError();
   return e == cudaSuccess ? 0 : ZS_ERR_LAUNCH;

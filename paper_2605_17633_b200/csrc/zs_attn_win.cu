@@ -596,7 +596,7 @@ int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, 
                     long long qus, long long kvus, int units, int heads, int S, int dh, const float* bh,
                     const float* bw, int bias_w, const int* q_sp, const int* k_sp, int b_row, int b_col, int prefix,
                     float tau, void* out, long long ldo, long long ous, const int* o_rows, long long bias_us,
-                    const __half* btab_ext, long long btab_us, cudaStream_t st) {
+                    const __half* btab_ext, long long btab_us, void* ws, size_t ws_bytes, cudaStream_t st) {
   using namespace attnw;
   if (S <= 0 || S > 256 || (b_row % 32) || (b_col % 32) || (dh != 64 && dh != 80)) return 1;
   if (bias_w > 16 || bias_w * bias_w != S || !(tau > 0.f)) return 1;
@@ -726,11 +726,13 @@ int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, 
   // followed by the [S, 32] one-hot key rows
   if (bias_us && !btab_ext && bias_us != (long long)heads * S * bias_w) return 1;
   const long long trows = btab_ext ? 0 : (long long)heads * S * (bias_us ? units : 1);
-  __half* btab = reinterpret_cast<__half*>(scratch(kScratchWinBias, (size_t)(trows + S) * 32 * sizeof(__half), st));
-  if (!btab) return ZS_ERR_DEVICE;
+  // caller-owned workspace (zs_stripe_attn_ws_bytes): fp16 operand rows + one-hot key rows
+  if (!ws || ws_bytes < (size_t)(trows + S) * 32 * sizeof(__half)) return ZS_ERR_WORKSPACE;
+  if (reinterpret_cast<uintptr_t>(ws) & 255) return ZS_ERR_ALIGN;
+  __half* btab = reinterpret_cast<__half*>(ws);
   {
     const long long n = (trows + S) * 32;
-    win_bias_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(bh, bw, trows, S, bias_w, 1.0f / tau, btab);
+    { win_bias_prep_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(bh, bw, trows, S, bias_w, 1.0f / tau, btab); count_launch(); }
   }
   p.btab = btab_ext ? btab_ext : btab;
   p.btab_us = btab_ext ? btab_us : (bias_us ? (long long)heads * S * 32 : 0);
@@ -762,7 +764,7 @@ int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, 
   const bool reg = max_live <= 3;
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], m[8], m[9], m[10], m[11], p);
+    { kern<<<grid, kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], m[8], m[9], m[10], m[11], p); count_launch(); }
   };
   if (dh == 64) {
     if (reg) launch(zs_attn_win_kernel<64, true>);

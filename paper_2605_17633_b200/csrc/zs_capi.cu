@@ -3,38 +3,15 @@
 // fc1+GELU -> fc2+scatter-add residual).
 #include <cudaTypedefs.h>
 
-#include <map>
 #include <mutex>
-#include <tuple>
 
 #include "zs_common.cuh"
 #include "zs_host.h"
 
 namespace zs {
 
-// Library-owned scratch (e.g. the attention kernels' fp16 bias-operand tables): one grow-only
-// buffer per (device, stream, slot), so calls on different streams never share it; guarded by a
-// mutex (the entry points are reentrant).  Growing frees the old buffer (cudaFree synchronises
-// the device, after which no kernel can still read it); steady-state calls allocate nothing.
-void* scratch(int slot, size_t bytes, cudaStream_t st) {
-  static std::mutex mu;
-  static std::map<std::tuple<int, cudaStream_t, int>, std::pair<void*, size_t>> bufs;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-  std::lock_guard<std::mutex> lock(mu);
-  auto& e = bufs[std::make_tuple(dev, st, slot)];
-  if (e.second < bytes) {
-    if (e.first) cudaFree(e.first);
-    e.first = nullptr;
-    e.second = 0;
-    if (cudaMalloc(&e.first, bytes) != cudaSuccess) return nullptr;
-    e.second = bytes;
-  }
-  return e.first;
-}
-
-
-
+static thread_local unsigned long long t_launches = 0;
+void count_launch() { ++t_launches; }
 
 int num_sms() {
   static int cached[64] = {0};
@@ -104,11 +81,14 @@ extern "C" const char* zs_status_string(int status) {
     case ZS_ERR_LAUNCH: return "CUDA kernel launch failed";
     case ZS_ERR_TMAP: return "cuTensorMapEncodeTiled rejected an operand";
     case ZS_ERR_DEVICE: return "no usable sm_100 device / driver entry point";
+    case ZS_ERR_WORKSPACE: return "workspace missing or smaller than the *_ws_bytes query";
     default: return "unknown zs_status";
   }
 }
 
-extern "C" int zs_abi_version(void) { return 100; }
+extern "C" int zs_abi_version(void) { return 200; }
+
+extern "C" unsigned long long zs_launch_counter(void) { return t_launches; }
 
 extern "C" int zs_gemm_bf16(int epi, const void* A, long long lda, const void* W, long long ldw, int M, int N,
                             int K, const float* bias, void* out, long long ld_out, const float* res,

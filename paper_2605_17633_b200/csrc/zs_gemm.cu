@@ -262,15 +262,15 @@ int launch_gemm(int epi, const void* A, long long lda, const void* W, long long 
   switch (epi) {
     case EPI_BF16:
       cudaFuncSetAttribute(zs_gemm_kernel<EPI_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-      zs_gemm_kernel<EPI_BF16><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep);
+      { zs_gemm_kernel<EPI_BF16><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep); count_launch(); }
       break;
     case EPI_BF16_GELU:
       cudaFuncSetAttribute(zs_gemm_kernel<EPI_BF16_GELU>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-      zs_gemm_kernel<EPI_BF16_GELU><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep);
+      { zs_gemm_kernel<EPI_BF16_GELU><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep); count_launch(); }
       break;
     case EPI_F32_RESID:
       cudaFuncSetAttribute(zs_gemm_kernel<EPI_F32_RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-      zs_gemm_kernel<EPI_F32_RESID><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep);
+      { zs_gemm_kernel<EPI_F32_RESID><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep); count_launch(); }
       break;
     default:
       return ZS_ERR_ARG;

@@ -436,15 +436,15 @@ int launch_gemm2(int epi, const void* A, long long lda, const void* W, long long
   switch (epi) {
     case 0:
       cudaFuncSetAttribute(zs_gemm2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-      zs_gemm2_kernel<0><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep);
+      { zs_gemm2_kernel<0><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep); count_launch(); }
       break;
     case 1:
       cudaFuncSetAttribute(zs_gemm2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-      zs_gemm2_kernel<1><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep);
+      { zs_gemm2_kernel<1><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep); count_launch(); }
       break;
     case 2:
       cudaFuncSetAttribute(zs_gemm2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-      zs_gemm2_kernel<2><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep);
+      { zs_gemm2_kernel<2><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep); count_launch(); }
       break;
     default:
       return ZS_ERR_ARG;

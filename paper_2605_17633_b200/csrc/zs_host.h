@@ -24,9 +24,8 @@ int launch_layernorm(const float* x, long long ldx, const int* rows, const int* 
                      const int* n_dev, int C, const float* g, const float* b, float eps, void* out, long long ldo,
                      int out_f32, cudaStream_t st);
 
-// Library-owned grow-only scratch per (device, stream, slot) (zs_capi.cu).
-void* scratch(int slot, size_t bytes, cudaStream_t st);
-enum ScratchSlot { kScratchWinBias = 0, kScratchGlobBias = 1 };
+// Kernel launches issued by the calling thread (zs_launch_counter, for the host's launch accounting).
+void count_launch();
 
 // Cached SM count of the current device.
 int num_sms();

@@ -228,8 +228,8 @@ extern "C" int zs_sobel_saliency(const float* x, int B, int H, int W, int C, int
   const int Hp = (H + window - 1) / window * window, Wp = (W + window - 1) / window * window;
   const int nwx = Wp / window;
   dim3 grid((Wp + order::TX - 1) / order::TX, (Hp + order::TY - 1) / order::TY, B);
-  sobel_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(x, H, W, C, window, Hp, Wp, nwx,
-                                                                          sal_glob, sal_win);
+  { sobel_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(x, H, W, C, window, Hp, Wp, nwx,
+                                                                          sal_glob, sal_win); count_launch(); }
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }
 
@@ -246,7 +246,7 @@ extern "C" int zs_rank_order(const float* scores, int scores_are_energy, int U, 
   if (smem > 200 * 1024) return ZS_ERR_SHAPE;
   cudaFuncSetAttribute(rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int threads = N >= 1024 ? 1024 : ((N + 31) / 32) * 32;
-  rank_kernel<<<U, threads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
-      scores, scores_are_energy, N, granularity, group_size, g, variant, morton_fwd, sigma, energy);
+  { rank_kernel<<<U, threads, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+      scores, scores_are_energy, N, granularity, group_size, g, variant, morton_fwd, sigma, energy); count_launch(); }
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }

@@ -293,7 +293,7 @@ int launch_relpos(const void* q, long long ldq, long long qus, int units, int he
   p.tx_a = BM * dh * 2;
   p.tx_b = nb * dh * 2;
   __nv_bfloat16* R = reinterpret_cast<__nv_bfloat16*>(ws);
-  relpos_table_kernel<<<(nb * dh + 255) / 256, 256, 0, st>>>(rel_h, rel_w, nr, dh, nb, R);
+  { relpos_table_kernel<<<(nb * dh + 255) / 256, 256, 0, st>>>(rel_h, rel_w, nr, dh, nb, R); count_launch(); }
   CUtensorMap m[4];
   const uint64_t ncol = (uint64_t)heads * dh;
   int rc = 0;
@@ -311,7 +311,7 @@ int launch_relpos(const void* q, long long ldq, long long qus, int units, int he
   if (grid > p.tiles) grid = p.tiles;
   auto launch = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<grid, n_threads(nb), smem, st>>>(m[0], m[1], m[2], m[3], p);
+    { kern<<<grid, n_threads(nb), smem, st>>>(m[0], m[1], m[2], m[3], p); count_launch(); }
   };
 #define ZS_RELPOS_DISPATCH(D)                                                          \
   if (nb == 64) {                                                                      \

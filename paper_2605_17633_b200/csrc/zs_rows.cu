@@ -106,9 +106,9 @@ int launch_layernorm(const float* x, long long ldx, const int* rows, const int* 
   const int nv = (C / 4 + 31) / 32;      // float4 per lane
 #define ZS_LN(NV)                                                                                          \
   if (out_f32)                                                                                             \
-    ln_rows_kernel<true, NV><<<grid, 256, 0, st>>>(x, ldx, rows, out_rows, n, n_dev, C, g, b, eps, out, ldo); \
+    { ln_rows_kernel<true, NV><<<grid, 256, 0, st>>>(x, ldx, rows, out_rows, n, n_dev, C, g, b, eps, out, ldo); count_launch(); } \
   else                                                                                                     \
-    ln_rows_kernel<false, NV><<<grid, 256, 0, st>>>(x, ldx, rows, out_rows, n, n_dev, C, g, b, eps, out, ldo);
+    { ln_rows_kernel<false, NV><<<grid, 256, 0, st>>>(x, ldx, rows, out_rows, n, n_dev, C, g, b, eps, out, ldo); count_launch(); }
   if (nv <= 2) {
     ZS_LN(2)
   } else if (nv <= 6) {
@@ -397,8 +397,8 @@ extern "C" int zs_permute_rows_f32(const float* src, float* dst, const int32_t* 
   if (!src || !dst || !map) return ZS_ERR_ARG;
   if (C <= 0 || C % 4) return ZS_ERR_SHAPE;
   if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) return ZS_ERR_ALIGN;
-  permute_rows_kernel<float4><<<grid_for_rows(rows_out, 8), 256, 0, S(stream)>>>(
-      reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), map, rows_out, C / 4);
+  { permute_rows_kernel<float4><<<grid_for_rows(rows_out, 8), 256, 0, S(stream)>>>(
+      reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), map, rows_out, C / 4); count_launch(); }
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }
 
@@ -408,8 +408,8 @@ extern "C" int zs_permute_rows_bf16(const void* src, void* dst, const int32_t* m
   if (!src || !dst || !map) return ZS_ERR_ARG;
   if (C <= 0 || C % 8) return ZS_ERR_SHAPE;
   if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) return ZS_ERR_ALIGN;
-  permute_rows_kernel<uint4><<<grid_for_rows(rows_out, 8), 256, 0, S(stream)>>>(
-      reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), map, rows_out, C / 8);
+  { permute_rows_kernel<uint4><<<grid_for_rows(rows_out, 8), 256, 0, S(stream)>>>(
+      reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), map, rows_out, C / 8); count_launch(); }
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }
 
@@ -419,8 +419,8 @@ extern "C" int zs_permute_rows_f32_bf16(const float* src, void* dst, const int32
   if (!src || !dst) return ZS_ERR_ARG;
   if (C <= 0 || C % 4) return ZS_ERR_SHAPE;
   if ((reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 7)) return ZS_ERR_ALIGN;
-  permute_f32_bf16_kernel<<<grid_for_rows(rows_out, 8), 256, 0, S(stream)>>>(
-      reinterpret_cast<const float4*>(src), reinterpret_cast<uint2*>(dst), map, rows_out, C / 4);
+  { permute_f32_bf16_kernel<<<grid_for_rows(rows_out, 8), 256, 0, S(stream)>>>(
+      reinterpret_cast<const float4*>(src), reinterpret_cast<uint2*>(dst), map, rows_out, C / 4); count_launch(); }
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }
 
@@ -435,13 +435,13 @@ extern "C" int zs_layout_maps(const int32_t* sigma_glob, const int32_t* sigma_lo
   const int grid = num_sms() * 4;
   if ((g_from_l || l_from_g) && (!sigma_glob || !sigma_loc || !s_from_l || !s_from_g || !l_from_s))
     return ZS_ERR_ARG;
-  if (sigma_loc) maps_local_kernel<<<grid, 256, 0, S(stream)>>>(sigma_loc, B, H, W, window, nwx, nwin, l_from_s,
-                                                                 s_from_l, l_is_pad);
+  if (sigma_loc) { maps_local_kernel<<<grid, 256, 0, S(stream)>>>(sigma_loc, B, H, W, window, nwx, nwin, l_from_s,
+                                                                 s_from_l, l_is_pad); count_launch(); }
   if (sigma_glob && (s_from_g || g_from_s))
-    maps_global_kernel<<<grid, 256, 0, S(stream)>>>(sigma_glob, B, HW, s_from_g, g_from_s);
+    { maps_global_kernel<<<grid, 256, 0, S(stream)>>>(sigma_glob, B, HW, s_from_g, g_from_s); count_launch(); }
   if (g_from_l || l_from_g)
-    maps_cross_kernel<<<grid, 256, 0, S(stream)>>>(sigma_glob, B, HW, nl, s_from_l, s_from_g, l_from_s, g_from_l,
-                                                    l_from_g);
+    { maps_cross_kernel<<<grid, 256, 0, S(stream)>>>(sigma_glob, B, HW, nl, s_from_l, s_from_g, l_from_s, g_from_l,
+                                                    l_from_g); count_launch(); }
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }
 
@@ -452,9 +452,9 @@ extern "C" int zs_unit_span_rows(int U, int S_, int k0, int k1, const uint8_t* i
   if (U <= 0) return 0;
   if (k0 < 0 || k1 < k0 || k1 > S_ || !rows || !unit_offsets) return ZS_ERR_ARG;
   const int grid = grid_for_rows(U, 8);
-  keep_count_kernel<<<grid, 256, 0, S(stream)>>>(U, S_, k0, k1, is_pad, unit_offsets);
-  keep_scan_kernel<<<1, 1024, 0, S(stream)>>>(U, unit_offsets);
-  keep_write_kernel<<<grid, 256, 0, S(stream)>>>(U, S_, k0, k1, is_pad, unit_offsets, rows);
+  { keep_count_kernel<<<grid, 256, 0, S(stream)>>>(U, S_, k0, k1, is_pad, unit_offsets); count_launch(); }
+  { keep_scan_kernel<<<1, 1024, 0, S(stream)>>>(U, unit_offsets); count_launch(); }
+  { keep_write_kernel<<<grid, 256, 0, S(stream)>>>(U, S_, k0, k1, is_pad, unit_offsets, rows); count_launch(); }
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }
 
@@ -468,11 +468,11 @@ extern "C" int zs_patchify(const float* img, int B, int Cin, int H, int W, int P
   if (B <= 0) return 0;
   if (!img || !out || P <= 0 || H % P || W % P) return ZS_ERR_SHAPE;
   if (P == 16 && (reinterpret_cast<uintptr_t>(img) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0)
-    patchify_vec_kernel<16><<<num_sms() * 8, 256, 0, S(stream)>>>(img, B, Cin, H, W,
-                                                                 reinterpret_cast<__nv_bfloat16*>(out));
+    { patchify_vec_kernel<16><<<num_sms() * 8, 256, 0, S(stream)>>>(img, B, Cin, H, W,
+                                                                 reinterpret_cast<__nv_bfloat16*>(out)); count_launch(); }
   else
-    patchify_kernel<<<num_sms() * 8, 256, 0, S(stream)>>>(img, B, Cin, H, W, P,
-                                                           reinterpret_cast<__nv_bfloat16*>(out));
+    { patchify_kernel<<<num_sms() * 8, 256, 0, S(stream)>>>(img, B, Cin, H, W, P,
+                                                           reinterpret_cast<__nv_bfloat16*>(out)); count_launch(); }
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }
 
@@ -480,8 +480,8 @@ extern "C" int zs_im2col3x3(const void* x, int B, int H, int W, int C, void* out
   if (B <= 0) return 0;
   if (!x || !out) return ZS_ERR_ARG;
   if (C % 8 || (reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(out)) & 15) return ZS_ERR_ALIGN;
-  im2col3x3_kernel<<<num_sms() * 8, 256, 0, S(stream)>>>(reinterpret_cast<const __nv_bfloat16*>(x), B, H, W, C,
-                                                          reinterpret_cast<__nv_bfloat16*>(out));
+  { im2col3x3_kernel<<<num_sms() * 8, 256, 0, S(stream)>>>(reinterpret_cast<const __nv_bfloat16*>(x), B, H, W, C,
+                                                          reinterpret_cast<__nv_bfloat16*>(out)); count_launch(); }
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }
 
@@ -490,7 +490,7 @@ extern "C" int zs_invert_rows(const int32_t* rows, long long n, const int32_t* n
   if (map_len <= 0) return 0;
   if (!map || (n > 0 && !rows)) return ZS_ERR_ARG;
   if (cudaMemsetAsync(map, 0xFF, (size_t)map_len * sizeof(int32_t), S(stream)) != cudaSuccess) return ZS_ERR_LAUNCH;
-  if (n > 0) invert_rows_kernel<<<grid_for_rows(n, 256), 256, 0, S(stream)>>>(rows, n, n_dev, map);
+  if (n > 0) { invert_rows_kernel<<<grid_for_rows(n, 256), 256, 0, S(stream)>>>(rows, n, n_dev, map); count_launch(); }
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }
 
@@ -501,8 +501,8 @@ extern "C" int zs_fill_flagged_rows_bf16(void* dst, long long ld, const void* sr
   if (ncol % 8 || ld % 8 || (reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src_row)) & 15)
     return ZS_ERR_ALIGN;
   const int nvec = ncol / 8;
-  fill_flagged_rows_kernel<<<num_sms() * 8, 256, 0, S(stream)>>>(reinterpret_cast<uint4*>(dst), ld / 8,
+  { fill_flagged_rows_kernel<<<num_sms() * 8, 256, 0, S(stream)>>>(reinterpret_cast<uint4*>(dst), ld / 8,
                                                                  reinterpret_cast<const uint4*>(src_row), flag, rows,
-                                                                 nvec);
+                                                                 nvec); count_launch(); }
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }

@@ -105,8 +105,19 @@ class StripeSortEncoder:
         self.has_local = "local" in cfg.layout
         self.has_global = "global" in cfg.layout
         self.tracer = NULL
+        # list -> (start, end) CUDA events of every block are appended to it (layout switch included)
+        self.block_events: list | None = None
 
     # ------------------------------------------------------------ workspace
+    def swap_state(self, state: tuple | None) -> tuple:
+        """Install ``state`` (None = fresh, empty) as this encoder's workspaces and return the
+        previous ones.  A CUDA graph records raw pointers, so GraphedImageEncoder captures with a
+        private state that later eager calls (another batch size, mode="dense", a larger keep
+        set) can neither reallocate nor share."""
+        old = (self._ws, self._ws_B)
+        self._ws, self._ws_B = state if state is not None else ({}, None)
+        return old
+
     def _workspace(self, B: int) -> dict:
         if self._ws_B == B:
             return self._ws
@@ -274,6 +285,10 @@ class StripeSortEncoder:
         layout = None
         for bi, blk in enumerate(self.params):
             kind = blk.kind
+            if self.block_events is not None:  # per-block device time (CostReport.ms, encoder.py:342,372)
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                ev[0].record()
+                self.block_events.append(ev)
             if kind != layout:
                 if layout is None:
                     src, mp = flat, (m["l_from_s"] if kind == "local" else m["g_from_s"])
@@ -288,6 +303,8 @@ class StripeSortEncoder:
             S = self.S2 if kind == "local" else self.HW
             Kc = RouterConfig(kf, cfg.bypass_mode).keep_count(S)
             self._block(blk, cur, od, B, r, rows[(kind, Kc)], ws, rows.get("nonpad") if kind == "local" else None)
+            if self.block_events is not None:
+                self.block_events[-1][1].record()
         if out is None:
             out = torch.empty((B * self.HW, cfg.d), device=self.device, dtype=torch.float32)
         with self.tracer.span("permute", bytes=out.numel() * 8):
@@ -318,6 +335,16 @@ class SparseSAMImageEncoder:
         # 3x3 neck conv weight [256, 256*9] (c, ky, kx) -> tap-major (ky, kx, c) to match im2col3x3
         self._neck2_tap = (frame.neck2_w.view(SAM_NECK, SAM_NECK, 3, 3).permute(0, 2, 3, 1)
                            .reshape(SAM_NECK, 9 * SAM_NECK).contiguous())
+
+    def swap_state(self, state: tuple | None) -> tuple:
+        """Frame buffers + the block stack's workspaces (see StripeSortEncoder.swap_state)."""
+        old = (getattr(self, "_bufs_d", None), self._buf_B, self.core.swap_state(None if state is None else state[2]))
+        if state is None:
+            self._bufs_d, self._buf_B = None, None
+        else:
+            self._bufs_d, self._buf_B = state[0], state[1]
+            # state[2] was installed above
+        return old
 
     def _bufs(self, B: int) -> dict:
         if self._buf_B != B:
@@ -373,9 +400,11 @@ class GraphedImageEncoder:
     """CUDA-graph replay of a :class:`SparseSAMImageEncoder` forward for a fixed batch size.
 
     The whole forward (patch embed, orderings, every block's ~9 launches, neck) has no host
-    synchronisation (device-side row counts, grow-only scratch), so it is captured once into a
-    CUDA graph over static input / output buffers and replayed: one graph launch instead of
+    synchronisation (device-side row counts, caller-owned workspaces), so it is captured once into
+    a CUDA graph over static input / output buffers and replayed: one graph launch instead of
     ~300 kernel launches from Python per call, which is what bounds small batches (one image).
+    The graph owns private workspaces (``swap_state``): eager calls on the same encoder before or
+    after the capture never reallocate or share the memory the graph replays into.
     """
 
     def __init__(self, enc: SparseSAMImageEncoder, batch: int, mode: str = "sparse"):
@@ -388,13 +417,17 @@ class GraphedImageEncoder:
         # stream), so everything the captured launches use is allocated before the capture
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream(dev))
-        with torch.cuda.stream(side):
-            for _ in range(2):
+        saved = enc.swap_state(None)
+        try:
+            with torch.cuda.stream(side):
+                for _ in range(2):
+                    enc(self.img, mode, out=self.out)
+            side.synchronize()
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=side):
                 enc(self.img, mode, out=self.out)
-        side.synchronize()
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph, stream=side):
-            enc(self.img, mode, out=self.out)
+        finally:
+            self._state = enc.swap_state(saved)  # the graph keeps its buffers alive, enc gets its own back
         torch.cuda.current_stream(dev).wait_stream(side)
 
     def __call__(self, img: torch.Tensor) -> torch.Tensor:

@@ -250,6 +250,7 @@ def stripe_attn(
     kv_unit_stride: int | None = None,
     o_rows: torch.Tensor | None = None,
     rel_pos: tuple[torch.Tensor, torch.Tensor] | None = None,
+    ws: torch.Tensor | None = None,
 ) -> torch.Tensor:
     """Block-sparse stripe attention.  q/k/v are row-major views ``[units*S, ld]``
     whose head ``h`` lives at columns ``h*dh``; ``out`` is ``[units*sq, heads*dh]``, or, with
@@ -258,7 +259,11 @@ def stripe_attn(
 
     Bias: ``bh``/``bw`` fp32 ``[heads, S, w]`` (one table pair, the reference's BiasTables) or
     ``[units, heads, S, w]`` (one pair per unit); or ``rel_pos=(rel_pos_h, rel_pos_w)`` (fp32
-    ``[2w-1, dh]``, bh = bw = None): SAM's q-dependent decomposed bias, computed on the fly."""
+    ``[2w-1, dh]``, bh = bw = None): SAM's q-dependent decomposed bias, computed on the fly.
+
+    ``ws``: the caller-owned uint8 workspace (``attn_ws_bytes`` / ``relpos_ws_bytes``); when None
+    one is taken from torch's stream-ordered caching allocator for this call (no sync, safe
+    across streams, kept alive by a CUDA graph that captures the call)."""
     for t, n in ((q, "q"), (k, "k"), (v, "v")):
         _need(t, torch.bfloat16, n)
         if t.stride(-1) != 1:
@@ -281,7 +286,7 @@ def stripe_attn(
         bias_w = (rh.shape[0] + 1) // 2
         if sq != sk or rh.shape != (2 * bias_w - 1, dh) or rw.shape != rh.shape:
             raise ValueError("rel_pos tables must be [2w-1, dh] with sq == sk == w*w")
-        ws = relpos_workspace(units, heads, sq, dh, bias_w, q.device)
+        ws = _workspace(ws, relpos_ws_bytes(units, heads, sq, dh, bias_w), q.device)
         _lib.call(
             "zs_stripe_attn_fwd_relpos", _ptr(q), _ptr(k), _ptr(v), ldq, ldk, ldv, qus, kvus, units, heads, sq, dh,
             _ptr(rh), _ptr(rw), bias_w, _ptr(q_sp), _ptr(k_sp), b_row, b_col, prefix, float(tau), _ptr(out),
@@ -296,41 +301,54 @@ def stripe_attn(
         if bh.shape[0] != units or bw.shape != bh.shape:
             raise ValueError("per-unit bias tables must be [units, heads, S, w]")
         bh, bw = bh.contiguous(), bw.contiguous()
+        ws = _workspace(ws, attn_ws_bytes(units, heads, sq, sk, dh, per_unit=True), q.device)
         _lib.call(
             "zs_stripe_attn_fwd_unit_bias", _ptr(q), _ptr(k), _ptr(v), ldq, ldk, ldv, qus, kvus, units, heads, sq, sk,
             dh, _ptr(bh), _ptr(bw), bh[0].numel(), bias_w, _ptr(q_sp), _ptr(k_sp), b_row, b_col, prefix, float(tau),
-            _ptr(out), out.stride(0), sq * out.stride(0), _ptr(o_rows) if o_rows is not None else None, _stream(),
+            _ptr(out), out.stride(0), sq * out.stride(0), _ptr(o_rows) if o_rows is not None else None, _ptr(ws),
+            ws.numel(), _stream(),
         )
         return out
+    ws = _workspace(ws, attn_ws_bytes(units, heads, sq, sk, dh), q.device)
     if o_rows is None:
         _lib.call(
             "zs_stripe_attn_fwd", _ptr(q), _ptr(k), _ptr(v), ldq, ldk, ldv, qus, kvus, units, heads, sq, sk, dh,
             _ptr(bh.contiguous()), _ptr(bw.contiguous()), bias_w, _ptr(q_sp), _ptr(k_sp), b_row, b_col, prefix,
-            float(tau), _ptr(out), out.stride(0), sq * out.stride(0), _stream(),
+            float(tau), _ptr(out), out.stride(0), sq * out.stride(0), _ptr(ws), ws.numel(), _stream(),
         )
     else:
         _lib.call(
             "zs_stripe_attn_fwd_rows", _ptr(q), _ptr(k), _ptr(v), ldq, ldk, ldv, qus, kvus, units, heads, sq, sk, dh,
             _ptr(bh.contiguous()), _ptr(bw.contiguous()), bias_w, _ptr(q_sp), _ptr(k_sp), b_row, b_col, prefix,
-            float(tau), _ptr(out), out.stride(0), sq * out.stride(0), _ptr(o_rows), _stream(),
+            float(tau), _ptr(out), out.stride(0), sq * out.stride(0), _ptr(o_rows), _ptr(ws), ws.numel(), _stream(),
         )
     return out
 
 
-_RELPOS_WS: dict = {}
+def attn_ws_bytes(units: int, heads: int, sq: int, sk: int, dh: int, per_unit: bool = False) -> int:
+    """Bytes of the attention's caller-owned workspace (zs_stripe_attn_ws_bytes)."""
+    return int(_lib.load().zs_stripe_attn_ws_bytes(units, heads, sq, sk, dh, 1 if per_unit else 0))
 
 
-def relpos_workspace(units: int, heads: int, S: int, dh: int, bias_w: int, device) -> torch.Tensor:
-    """Grow-only per-device workspace of the SAM rel-pos path (zs_relpos_ws_bytes)."""
+def relpos_ws_bytes(units: int, heads: int, S: int, dh: int, bias_w: int) -> int:
+    """Bytes of the SAM rel-pos path's caller-owned workspace (zs_relpos_ws_bytes)."""
     need = int(_lib.load().zs_relpos_ws_bytes(units, heads, S, dh, bias_w))
     if need <= 0:
-        raise ValueError(f"rel-pos mode unsupported for S={S}, dh={dh}, w={bias_w}")
-    key = torch.device(device)
-    ws = _RELPOS_WS.get(key)
-    if ws is None or ws.numel() < need:
-        ws = torch.empty(need, dtype=torch.uint8, device=key)
-        _RELPOS_WS[key] = ws
-    return ws
+        raise ValueError(f"rel-pos shape unsupported (dh={dh}, w={bias_w})")
+    return need
+
+
+def _workspace(ws: torch.Tensor | None, need: int, device) -> torch.Tensor:
+    """The caller's workspace if large enough, else a fresh one from the caching allocator
+    (allocated on the current stream; its 256-byte alignment is what the library requires)."""
+    if ws is not None:
+        _need(ws, torch.uint8, "ws")
+        if ws.numel() < need:
+            raise ValueError(f"workspace has {ws.numel()} bytes, the call needs {need}")
+        if ws.data_ptr() % 256:
+            raise ValueError("workspace must be 256-byte aligned")
+        return ws
+    return torch.empty(max(need, 256), dtype=torch.uint8, device=device)
 
 
 def relpos_bias(q: torch.Tensor, *, units: int, heads: int, S: int, dh: int, rel_pos_h: torch.Tensor,
@@ -345,7 +363,7 @@ def relpos_bias(q: torch.Tensor, *, units: int, heads: int, S: int, dh: int, rel
     w = (rh.shape[0] + 1) // 2
     bh = torch.empty((units, heads, S, w), device=q.device, dtype=torch.float32)
     bw = torch.empty_like(bh)
-    ws = relpos_workspace(units, heads, S, dh, w, q.device)
+    ws = _workspace(None, relpos_ws_bytes(units, heads, S, dh, w), q.device)
     qus = q_unit_stride if q_unit_stride is not None else S * q.stride(0)
     _lib.call("zs_relpos_bias", _ptr(q), q.stride(0), qus, units, heads, S, dh, w, _ptr(rh), _ptr(rw), _ptr(q_sp),
               _ptr(bh), _ptr(bw), _ptr(ws), ws.numel(), _stream())

@@ -35,6 +35,8 @@ if "stripes" in sys.argv:  # σ made of the 4 (y % 2, x % 2) parity classes, eac
     key = cls[None, :].float() * 2 + torch.rand(U, S, device="cuda")
     sp = torch.argsort(key, dim=1).int().contiguous()
 outs = {n: torch.empty(U * S, C, device="cuda", dtype=torch.bfloat16) for n in libs}
+wsn = _lib.load().zs_stripe_attn_ws_bytes(U, H, S, S, dh, 0)
+ws = {n: torch.empty(wsn, device="cuda", dtype=torch.uint8) for n in libs}
 st = torch.cuda.current_stream().cuda_stream
 
 
@@ -44,18 +46,19 @@ if ROWS:
     orows = torch.where(keep, torch.cumsum(keep.int(), 0) - 1, torch.full_like(keep, -1, dtype=torch.long)).int()
 
 
-def call(lib, out):
+def call(lib, out, name):
     q = qkv
     if ROWS:
         rc = lib.zs_stripe_attn_fwd_rows(q.data_ptr(), q.data_ptr() + 2 * C, q.data_ptr() + 4 * C, 3 * C, 3 * C,
                                          3 * C, S * 3 * C, S * 3 * C, U, H, S, S, dh, bh.data_ptr(), bw.data_ptr(), w,
                                          sp.data_ptr(), sp.data_ptr(), tile, tile, p, dh ** -0.5, out.data_ptr(), C,
-                                         S * C, orows.data_ptr(), st)
+                                         S * C, orows.data_ptr(), ws[name].data_ptr(), wsn, st)
         assert rc == 0, rc
         return
     rc = lib.zs_stripe_attn_fwd(q.data_ptr(), q.data_ptr() + 2 * C, q.data_ptr() + 4 * C, 3 * C, 3 * C, 3 * C,
                                 S * 3 * C, S * 3 * C, U, H, S, S, dh, bh.data_ptr(), bw.data_ptr(), w, sp.data_ptr(),
-                                sp.data_ptr(), tile, tile, p, dh ** -0.5, out.data_ptr(), C, S * C, st)
+                                sp.data_ptr(), tile, tile, p, dh ** -0.5, out.data_ptr(), C, S * C, ws[name].data_ptr(),
+                                wsn, st)
     assert rc == 0, rc
 
 
@@ -66,7 +69,7 @@ PAIRS = 20  # paired, finely interleaved samples: the power-capped clock drifts 
 def batch(name, n=4):
     e0.record()
     for _ in range(n):
-        call(libs[name], outs[name])
+        call(libs[name], outs[name], name)
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / n
@@ -74,7 +77,7 @@ def batch(name, n=4):
 
 for name in libs:
     for _ in range(2):
-        call(libs[name], outs[name])
+        call(libs[name], outs[name], name)
 torch.cuda.synchronize()
 ratios, tn, to = [], [], []
 for i in range(PAIRS):
