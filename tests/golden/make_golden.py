@@ -150,6 +150,25 @@ def config1_blocks():
     save("config1_blocks", **out)
 
 
+def attention_global():
+    """Global-attention shapes of SAM ViT-B/H (S = 4096 = 64x64, tile 128): one head each, the
+    reference's own ashape_attention output.  Inputs come from zstripe.Rng(seed) (regenerated in
+    the tests by the oracle's bit-exact SplitMix), only the key permutation and outputs are stored."""
+    d = {}
+    for ci, (dh, r, seed) in enumerate([(80, 0.4, 31), (64, 0.25, 32)]):
+        g = Z.Rng(seed)
+        q, k, v = g.normal((4096, dh)), g.normal((4096, dh)), g.normal((4096, dh))
+        bh, bw = g.normal((4096, 64), std=0.5), g.normal((4096, 64), std=0.5)
+        sp = np.random.default_rng(seed).permutation(4096)
+        t = time.time()
+        out = Z.ashape_attention(q, k, v, Z.BiasTables(bh, bw), Z.Permutation(sp), Z.Permutation(sp),
+                                 Z.AShapeConfig(128, 128, r))
+        print(f"global attention dh={dh} r={r}: {time.time() - t:.1f} s")
+        d.update({f"g{ci}_meta": np.array([dh, int(r * 1000), seed]), f"g{ci}_sp": sp.astype(np.int16),
+                  f"g{ci}_out": out})
+    save("attention_global", **d)
+
+
 def sptn_files():
     """SPTN files written by the reference (tensor.py:65-84, grid.py:122-127) for the reader/writer gate."""
     d = OUT / "sptn"
@@ -162,7 +181,7 @@ def sptn_files():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["grid", "c1orders", "attn", "mlp", "enc", "c1blocks", "sptn"]
+    which = sys.argv[1:] or ["grid", "c1orders", "attn", "mlp", "enc", "c1blocks", "sptn", "attn_global"]
     if "sptn" in which:
         sptn_files()
     if "grid" in which:
@@ -177,3 +196,5 @@ if __name__ == "__main__":
         encoder_small()
     if "c1blocks" in which:
         config1_blocks()
+    if "attn_global" in which:
+        attention_global()

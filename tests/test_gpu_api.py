@@ -133,3 +133,15 @@ def test_cost_report_matches_reference_accounting():
     assert mine[0] == ref[0]
     for a, b in zip(mine[1:], ref[1:]):
         assert a.rsplit(",", 1)[0] == b.rsplit(",", 1)[0]
+
+
+@pytest.mark.parametrize("ci", [0, 1])
+def test_global_attention_vs_reference_golden(ci):
+    """S = 4096 global heads (dh 80 / 64, tile 128) straight against the reference's own output
+    (tests/golden/attention_global.npz), not only the oracle."""
+    from test_oracle_golden import _global_case
+
+    q, k, v, bh, bw, sp, r, ref = _global_case(golden("attention_global"), ci)
+    got = api.ashape_attention(q, k, v, api.BiasTables(bh, bw), sp, sp, Z.AShapeConfig(b_row=128, b_col=128, r=r))
+    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert rel <= 1e-2 and np.abs(got - ref).max() <= 3e-2, (rel, np.abs(got - ref).max())

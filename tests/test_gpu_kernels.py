@@ -383,8 +383,9 @@ def test_attention_output_row_map_and_pad_helpers():
 
 @pytest.mark.parametrize("S,w,tile", [(196, 14, 32), (4096, 64, 128)])
 def test_attention_concurrent_streams(S, w, tile):
-    """Two streams run the attention at once with different bias tables: the library's bias-
-    operand scratch is per (device, stream), so each result equals its own sequential run."""
+    """Two streams run the attention at once with different bias tables: each call's bias-operand
+    workspace comes from the stream-ordered caching allocator (the library owns none), so each
+    result equals its own sequential run."""
     g = torch.Generator().manual_seed(21)
     units, heads, dh = (40 if S <= 256 else 2), 2, 80
     C = heads * dh

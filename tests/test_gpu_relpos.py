@@ -200,3 +200,29 @@ def test_encoder_rel_pos_mode_vs_fp32_twin(side):
     ref = _twin_blocks(x, params, cfg).double()
     cos = float((got * ref).sum() / (got.norm() * ref.norm()))
     assert cos >= 0.999 and rel(got, ref) <= 3e-2, (cos, rel(got, ref))
+
+
+@pytest.mark.parametrize("S,w,tile", [(196, 14, 32), (4096, 64, 128)])
+def test_relpos_attention_concurrent_streams(S, w, tile):
+    """the SAM rel-pos path on two streams at once (different rel-pos tables) — every
+    call takes its own workspace (caller-owned / stream-ordered allocator), so each result equals
+    its sequential run."""
+    units, heads, dh = (18 if S <= 256 else 2), 2, 80
+    qkv, rh, rw, sp = make_case(units, heads, S, dh, w, seed=77)
+    rh2, rw2 = rh.flip(0).contiguous(), (rw * 1.5).contiguous()
+    C = heads * dh
+    kw = dict(units=units, heads=heads, sq=S, sk=S, dh=dh, q_sp=sp, k_sp=sp, b_row=tile, b_col=tile, prefix=2,
+              tau=dh ** -0.5, bh=None, bw=None)
+    tabs = [(rh, rw), (rh2, rw2)]
+    ref = [K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], rel_pos=t, **kw) for t in tabs]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    outs = [torch.empty_like(r) for r in ref]
+    for _ in range(3):
+        for s_, t, o in zip(streams, tabs, outs):
+            s_.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s_):
+                K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], rel_pos=t, out=o, **kw)
+        torch.cuda.synchronize()
+        for o, r in zip(outs, ref):
+            assert torch.equal(o, r)

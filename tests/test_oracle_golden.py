@@ -190,3 +190,37 @@ def test_schedule_table_survey_8d():
     for d, (pl, pg, kl, kg) in table.items():
         assert math.floor(d * 7) == pl and math.floor(d * 32) == pg
         assert O.keep_count(d, 196) == kl and O.keep_count(d, 4096) == kg
+
+
+def _global_case(g, ci):
+    dh, rm, seed = g[f"g{ci}_meta"].tolist()
+    rng = O.SplitMix(seed)
+    q, k, v = rng.normal((4096, dh)), rng.normal((4096, dh)), rng.normal((4096, dh))
+    bh, bw = rng.normal((4096, 64), std=0.5), rng.normal((4096, 64), std=0.5)
+    return q, k, v, bh, bw, g[f"g{ci}_sp"].astype(np.int64), rm / 1000, g[f"g{ci}_out"]
+
+
+@pytest.mark.parametrize("ci", [0, 1])
+def test_global_attention_golden(ci):
+    """SAM global-attention shape (S = 4096, tile 128, dh 80 / 64): the oracle's streaming
+    attention (BLAS matmul) vs the reference's own output."""
+    q, k, v, bh, bw, sp, r, ref = _global_case(golden("attention_global"), ci)
+    out = O.ashape_attention(q, k, v, bh, bw, sp, sp, 128, 128, r)
+    np.testing.assert_allclose(out, ref, rtol=0, atol=2e-5)
+
+
+def test_masked_attention_f64_pinned_to_reference():
+    """The float64 masked-softmax checker the 4096-token / ViT-H GPU tests use is itself pinned to
+    the reference's outputs: every attention golden (5 small cases x 4 densities, 2 global heads)."""
+    g = golden("attention_cases")
+    for ci in range(5):
+        sq, w, dh, br, bc = g[f"c{ci}_shape"].tolist()
+        for r in (0.0, 0.25, 0.4, 1.0):
+            out = O.masked_attention_f64(g[f"c{ci}_q"], g[f"c{ci}_k"], g[f"c{ci}_v"], g[f"c{ci}_bh"], g[f"c{ci}_bw"],
+                                         g[f"c{ci}_sp"], g[f"c{ci}_kp"], br, bc, r)
+            np.testing.assert_allclose(out, g[f"c{ci}_r{int(r * 100)}"], rtol=0, atol=5e-6)
+    gg = golden("attention_global")
+    for ci in range(2):
+        q, k, v, bh, bw, sp, r, ref = _global_case(gg, ci)
+        out = O.masked_attention_f64(q, k, v, bh, bw, sp, sp, 128, 128, r)
+        np.testing.assert_allclose(out, ref, rtol=0, atol=2e-5)
