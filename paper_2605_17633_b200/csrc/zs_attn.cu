@@ -962,7 +962,8 @@ extern "C" int zs_stripe_attn_fwd_relpos(const void* q, const void* k, const voi
     if (rc == 0) {
       rc = attn_dispatch(q, k, v, ldq, ldk, ldv, q_unit_stride, kv_unit_stride, units, heads, S, S, dh, nullptr,
                          nullptr, 0, bias_w, q_sp, k_sp, b_row, b_col, prefix_tiles, tau, out, ldo, o_unit_stride,
-                         o_rows, btab, us, nullptr, 0, st);
+                         o_rows, btab, us, tables + relpos_tables_bytes(units, heads, S, bias_w),
+                         attn_ws_bytes(units, heads, S, S, 1), st);
       if (rc <= 0) return rc;
     }
   }

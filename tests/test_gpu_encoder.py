@@ -183,7 +183,7 @@ def depth_metrics(got, ref):
 # Full-depth tolerance: the bf16 error compounds over 24 / 32 blocks, so on top of the
 # cosine / Frobenius / per-token bounds the largest element error is bounded relative to the output's
 # own scale: max|got - ref| <= MAX_ABS_REL * max|ref|.
-MAX_ABS_REL = 0.05
+MAX_ABS_REL = 0.02  # measured r2: ViT-H 32 blocks 0.0054, ViT-L 24 blocks 0.0061-0.0062
 
 
 @pytest.mark.parametrize("model,density", [("vit_h", 0.4), ("vit_l", 0.4), ("vit_l", 0.3)])
