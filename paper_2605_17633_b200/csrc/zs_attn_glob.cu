@@ -15,9 +15,11 @@
 //    the softmax.  All 8 softmax warps work on every chunk: the two warps of a TMEM lane
 //    quarter (warps 4 + q and 8 + q) split its 128 keys (64 each) and exchange partial row
 //    maxima through shared memory (one 64-thread named barrier per chunk).
-//  * P (bf16) overwrites the chunk's S columns in TMEM and is the A operand of the PV MMA.  One
-//    O accumulator per CTA; the PV MMA also multiplies P by a ones matrix into 16 extra O
-//    columns, which hold the row sums (of the bf16 P exactly as applied to V).
+//  * P (bf16) overwrites the chunk's S columns in TMEM (half w's 64 keys at columns [64w, 64w+32),
+//    inside its own S columns) and is the A operand of the PV MMA.  One O accumulator per CTA;
+//    the PV is ONE N = DH + 16 MMA per 16 keys: V is staged as MN-major SW32 atoms of 16 columns
+//    followed by an atom of bf16 ones, so the 16 extra O columns hold the row sums (of the bf16 P
+//    exactly as applied to V).  (N = 16 MMAs cost ~26 cycles each, as much as N = 64.)
 //  * Lazy rescaling: O (and its row-sum columns) is rescaled in TMEM, warp-wide, only when a
 //    row max grows by more than ln 256.
 //  * The next item's Bq rows are prefetched from the fp16 table one item ahead and written into
@@ -46,6 +48,7 @@ constexpr uint32_t TM_S = 0;     // S_w at [w*128, w*128+128)
 constexpr uint32_t TM_O = 256;   // O at [256, 256 + DH), row sums (ones MMA) at [256 + DH, +16)
 constexpr uint32_t TM_BQ = 416;  // Bq: 128 fp16 = 64 columns
 constexpr int OH_BYTES = 2 * BQ * 128;  // two 64-column SW128 slabs (e_ky | e_kx)
+constexpr int VATOM = BQ * 32;          // V: MN-major SW32 atoms of 16 columns x 128 keys
 
 struct Params {
   int units, heads, S, bias_w, T, prefix, items;
@@ -57,7 +60,7 @@ struct Params {
   const int* k_sp;
   float tau;
   __nv_bfloat16* out;
-  int off_q, off_k, off_oh, off_v, off_ml, off_ones, off_bar, tile;
+  int off_q, off_k, off_oh, off_v, off_ml, off_bar, tile, vstage;
   int trace;
 };
 
@@ -66,10 +69,18 @@ struct Shape {
   static constexpr bool kTail = DH == 80;
   static constexpr int MAIN = BQ * 128;
   static constexpr int TILE = ((MAIN + (kTail ? BQ * 32 : 0) + 1023) / 1024) * 1024;
+  // V stage: DH/16 column atoms + one atom of bf16 ones (row sums): the PV MMA is ONE N = DH + 16
+  // instruction per 16 keys (an N = 16 MMA costs ~26 cycles, as much as N = 64: tools/glob_mma_bench.cu)
+  static constexpr int VSTAGE = (DH / 16 + 1) * VATOM;
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
 }
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -168,7 +179,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tq);
     tma_prefetch_desc(&tk);
-    tma_prefetch_desc(&tv);
+    tma_prefetch_desc(&tv_t);
     for (int s = 0; s < QST; ++s) {
       mbar_init(&q_full[s], 1);
       mbar_init(&q_empty[s], 1);
@@ -233,9 +244,9 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
               const int s = c % VST;
               mbar_wait_sleep(&v_empty[s], ((c / VST) & 1) ^ 1);
               mbar_expect_tx(&v_full[s], BQ * DH * 2);
-              uint8_t* vv = smem + P.off_v + s * L::TILE;
-              tma_load_3d(vv, &tv, &v_full[s], col, cj * BQ, u);
-              if constexpr (kTail) tma_load_3d(vv + L::MAIN, &tv_t, &v_full[s], col + 64, cj * BQ, u);
+              uint8_t* vv = smem + P.off_v + s * L::VSTAGE;
+#pragma unroll
+              for (int a = 0; a < DH / 16; ++a) tma_load_3d(vv + a * VATOM, &tv_t, &v_full[s], col + 16 * a, cj * BQ, u);
             }
           }
         }
@@ -244,14 +255,12 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       // ---------------------------------------------------------- MMA issuer (whole warp)
       constexpr uint32_t id_s = idesc_bf16(BQ, BQ);
       constexpr uint32_t id_b = idesc_f16(BQ, BQ);
-      constexpr uint32_t id_pv = idesc_bf16(BQ, 64, false, true);
-      constexpr uint32_t id_pv2 = idesc_bf16(BQ, 16, false, true);
+      constexpr uint32_t id_pv = idesc_bf16(BQ, DH + 16, false, true);
       constexpr uint32_t TILE16 = L::TILE >> 4;
       const uint64_t dq = sdesc_k_sw128(smem + P.off_q), dqt = sdesc_k_sw32(smem + P.off_q + L::MAIN);
       const uint64_t dk = sdesc_k_sw128(smem + P.off_k), dkt = sdesc_k_sw32(smem + P.off_k + L::MAIN);
       const uint64_t doh = sdesc_k_sw128(smem + P.off_oh);
-      const uint64_t dv = sdesc_mn_sw128(smem + P.off_v), dvt = sdesc_mn_sw32(smem + P.off_v + L::MAIN);
-      const uint64_t dones = sdesc_mn_sw32(smem + P.off_ones);
+      const uint64_t dv = sdesc(smem + P.off_v, VATOM, 256, 6);  // MN-major SW32 atoms, LBO = one atom
       // S'(c) of chunk ordinal c into S_w: q.k (bf16) then + Bq . OH^T (fp16, A from TMEM)
       int first_c = 0;  // chunk ordinal of the current item's first chunk (trace only)
       auto issue_s = [&](int c, int k, int w, bool last) {
@@ -285,16 +294,13 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         const int vs = c % VST;
         mbar_wait(&v_full[vs], (c / VST) & 1);
         tc_fence_after();
-        const uint64_t v = dv + vs * TILE16, vt = dvt + vs * TILE16;
+        const uint64_t v = dv + vs * (L::VSTAGE >> 4);
         const uint32_t a0 = tmem + TM_S + w * 128;
         const uint32_t d = tmem + TM_O;
+        // [O | row sums] (+)= P . [V | 1]: one N = DH + 16 MMA per 16 keys
 #pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks) {
-          const uint32_t acc = (!first || ks > 0) ? 1u : 0u;
-          umma_ts(d, a0 + 8 * ks, v + ks * (16 * 128 / 16), id_pv, acc);
-          if constexpr (kTail) umma_ts(d + 64, a0 + 8 * ks, vt + ks * (16 * 32 / 16), id_pv2, acc);
-          umma_ts(d + DH, a0 + 8 * ks, dones + ks * (16 * 32 / 16), id_pv2, acc);  // row sums of P
-        }
+        for (int ks = 0; ks < BQ / 16; ++ks)
+          umma_ts(d, a0 + 8 * ks + (ks >= 4 ? 32 : 0), v + ks * (16 * 32 / 16), id_pv, (!first || ks > 0) ? 1u : 0u);
         umma_commit_elect(o_full);
         umma_commit_elect(&v_empty[vs]);
       };
@@ -348,12 +354,14 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       const uint32_t one = 0x3C00u;  // fp16 1.0
       const int kbase = (warp - 2) * 64;
       const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
-      {  // bf16 ones [128, 16] (every element 1.0, so the swizzle is irrelevant); published to the
-         // tensor core by the fence before the first oh_full arrive
+      {  // the ones atom of every V stage: bf16 ones [128 keys, 16] (every element 1.0, so the swizzle
+         // is irrelevant); published to the tensor core by the fence before the first oh_full arrive
         const uint4 o4 = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          reinterpret_cast<uint4*>(smem + P.off_ones)[((warp - 2) * 32 + lane) * 4 + q] = o4;
+        for (int s = 0; s < VST; ++s)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            reinterpret_cast<uint4*>(smem + P.off_v + s * P.vstage + (DH / 16) * VATOM)[((warp - 2) * 32 + lane) * 4 + q] = o4;
       }
 #pragma unroll
       for (int st = 0; st < OST; ++st)
@@ -575,19 +583,32 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
           for (int jj = 0; jj < 64; ++jj)
             if (jj >= kvalid) sr[jj] = __float_as_uint(-INFINITY);
         }
-        float m0 = __uint_as_float(sr[0]), m1 = __uint_as_float(sr[1]);
+        // P of this half's 64 keys against reference mref -> TMEM columns [64w, 64w + 32) (the half's
+        // own S columns, already in registers: no hazard with the partner half)
+        auto emit = [&](float mref) {
+          const float mc = (mref == -INFINITY) ? 0.f : mref * L2E;
+          const unsigned long long c2 = f32x2(cexp, cexp), m2 = f32x2(-mc, -mc);
 #pragma unroll
-        for (int jj = 2; jj < 64; jj += 2) {
-          m0 = fmaxf(m0, __uint_as_float(sr[jj]));
-          m1 = fmaxf(m1, __uint_as_float(sr[jj + 1]));
+          for (int g = 0; g < 2; ++g) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              pk[q] = exp2_pair_bf16_ns(__uint_as_float(sr[32 * g + 2 * q]), __uint_as_float(sr[32 * g + 2 * q + 1]),
+                                        c2, m2);
+            }
+            tmem_st16(s_addr + 64 * w + 16 * g, pk);  // P (bf16) of keys [64w + 32g, +32)
+          }
+        };
+        float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+        for (int jj = 0; jj < 64; jj += 4) {
+          m0 = max3f(m0, __uint_as_float(sr[jj]), __uint_as_float(sr[jj + 1]));
+          m1 = max3f(m1, __uint_as_float(sr[jj + 2]), __uint_as_float(sr[jj + 3]));
         }
-        // partial max -> partner half; after this barrier both halves' S loads are complete,
-        // so P may overwrite S columns of either half
+        // partial max -> partner half
         const float mp = fmaxf(m0, m1);
         xch[(buf * 2 + w) * BQ + r] = mp;
-        tc_fence_before();
         named_bar_sync(pair_bar, 64);
-        tc_fence_after();
         const float mx = tau * fmaxf(mp, xch[(buf * 2 + (w ^ 1)) * BQ + r]);  // row max logit
         // lazy rescale (identical decision in both halves): a warp-wide TMEM round trip when any
         // row of the warp moves its reference, alpha = 1 for the others
@@ -602,17 +623,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
           }
           if (upd) m_ref = mx;
         }
-        const float mc = (m_ref == -INFINITY) ? 0.f : m_ref * L2E;
-        const unsigned long long c2 = f32x2(cexp, cexp), m2 = f32x2(-mc, -mc);
-#pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int q = 0; q < 16; ++q)
-            pk[q] = exp2_pair_bf16_ns(__uint_as_float(sr[32 * g + 2 * q]), __uint_as_float(sr[32 * g + 2 * q + 1]),
-                                      c2, m2);
-          tmem_st16(s_addr + 32 * w + 16 * g, pk);  // P (bf16) of keys [64w + 32g, +32)
-        }
+        emit(m_ref);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -716,6 +727,7 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
   p.trace = getenv("ZS_GLOB_TRACE") ? 1 : 0;
   const int tile = dh == 80 ? Shape<80>::TILE : Shape<64>::TILE;
   p.tile = tile;
+  p.vstage = dh == 80 ? Shape<80>::VSTAGE : Shape<64>::VSTAGE;
   int off = 0;
   auto take = [&](int bytes, int align) {
     off = (off + align - 1) / align * align;
@@ -726,9 +738,8 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
   p.off_q = take(QST * tile, 1024);
   p.off_k = take(KST * tile, 1024);
   p.off_oh = take(OST * OH_BYTES, 1024);
-  p.off_v = take(VST * tile, 1024);
+  p.off_v = take(VST * p.vstage, 1024);
   p.off_ml = take(2 * 4 * BQ * 4, 16);
-  p.off_ones = take(BQ * 32, 1024);  // [128 keys, 16] bf16 ones: B operand of the row-sum MMA
   p.off_bar = take(512, 8);
   const size_t smem = 1024 + (size_t)off;
   if (smem > 227 * 1024) return 1;
@@ -754,14 +765,14 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
   rc |= make_tmap_3d_bf16(&m[0], q, ncol, S, units, ldq, qus, 64, BQ, 1, CU_TENSOR_MAP_SWIZZLE_128B);
   rc |= make_tmap_3d_bf16(&m[2], k, ncol, S, units, ldk, kvus, 64, BQ, 1, CU_TENSOR_MAP_SWIZZLE_128B);
   rc |= make_tmap_3d_bf16(&m[4], v, ncol, S, units, ldv, kvus, 64, BQ, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+  // V: 16-column SW32 boxes only (the PV B operand is a row of MN-major SW32 atoms)
+  rc |= make_tmap_3d_bf16(&m[5], v, ncol, S, units, ldv, kvus, 16, BQ, 1, CU_TENSOR_MAP_SWIZZLE_32B);
   if (dh == 80) {
     rc |= make_tmap_3d_bf16(&m[1], q, ncol, S, units, ldq, qus, 16, BQ, 1, CU_TENSOR_MAP_SWIZZLE_32B);
     rc |= make_tmap_3d_bf16(&m[3], k, ncol, S, units, ldk, kvus, 16, BQ, 1, CU_TENSOR_MAP_SWIZZLE_32B);
-    rc |= make_tmap_3d_bf16(&m[5], v, ncol, S, units, ldv, kvus, 16, BQ, 1, CU_TENSOR_MAP_SWIZZLE_32B);
   } else {
     m[1] = m[0];
     m[3] = m[2];
-    m[5] = m[4];
   }
   if (rc) return ZS_ERR_TMAP;
   int grid = num_sms();

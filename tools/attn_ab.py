@@ -12,8 +12,11 @@ import torch
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2605_17633_b200 import _lib  # noqa: E402
 
-libs = {name: ctypes.CDLL(str(Path(_lib.LIB_PATH).parent / f)) for name, f in
-        [("new", "libzstripe_b200.so"), ("old", "libzstripe_b200_old.so")]}
+import os  # noqa: E402
+# ZS_AB_LIBS="a.so,b.so,...": variants in _lib/ timed against the first (default: new vs _old)
+_names = os.environ.get("ZS_AB_LIBS", "libzstripe_b200.so,libzstripe_b200_old.so").split(",")
+libs = {("new" if i == 0 else ("old" if i == 1 else f)): ctypes.CDLL(str(Path(_lib.LIB_PATH).parent / f))
+        for i, f in enumerate(_names)}
 for l in libs.values():
     l.zs_stripe_attn_fwd.argtypes = _lib.SIGNATURES["zs_stripe_attn_fwd"]
     l.zs_stripe_attn_fwd_rows.argtypes = _lib.SIGNATURES["zs_stripe_attn_fwd_rows"]
@@ -79,17 +82,17 @@ for name in libs:
     for _ in range(2):
         call(libs[name], outs[name], name)
 torch.cuda.synchronize()
-ratios, tn, to = [], [], []
+names = list(libs)
+times = {n: [] for n in names}
 for i in range(PAIRS):
-    order = ("new", "old") if i % 2 == 0 else ("old", "new")
-    t = {name: batch(name) for name in order}
-    ratios.append(t["new"] / t["old"])
-    tn.append(t["new"])
-    to.append(t["old"])
-for v in (ratios, tn, to):
-    v.sort()
+    order = names if i % 2 == 0 else names[::-1]
+    for name in order:
+        times[name].append(batch(name))
 m = PAIRS // 2
-print(f"{kind} new/old median {ratios[m]:.4f} (q1 {ratios[PAIRS // 4]:.4f} q3 {ratios[3 * PAIRS // 4]:.4f})  "
-      f"new {tn[m]:.3f} ms  old {to[m]:.3f} ms", flush=True)
-d = (outs["new"].float() - outs["old"].float()).norm() / outs["old"].float().norm()
-print("rel diff new vs old:", d.item())
+ref = sorted(times["old"])[m]
+for name in names:
+    r = sorted(a / b for a, b in zip(times[name], times["old"]))
+    print(f"{kind} {name:>28s}: median {sorted(times[name])[m]:.3f} ms  vs old {r[m]:.4f} "
+          f"(q1 {r[PAIRS // 4]:.4f} q3 {r[3 * PAIRS // 4]:.4f})", flush=True)
+    d = (outs[name].float() - outs["old"].float()).norm() / outs["old"].float().norm()
+    print(f"   rel diff vs old: {d.item():.3e}")
