@@ -457,3 +457,134 @@ def encoder_forward(x, weights, cfg: EncoderConfig, mode: str = "sparse"):
     enc.block_events = None
     y = y[0] if single else y
     return _like(y, x), cost_report(cfg, mode, per)
+
+
+# ---------------------------------------------------------------- benchmarks (encoder.py:388-444, cli.py:96-130)
+@dataclass(frozen=True)
+class BenchRow:
+    density: float
+    achieved_density: float
+    median_ms: float
+    speedup: float
+
+
+BENCH_COLUMNS = "density,achieved_density,median_ms,speedup"
+
+
+def _median(v):
+    s = sorted(v)
+    n = len(s)
+    return s[n // 2] if n % 2 else 0.5 * (s[n // 2 - 1] + s[n // 2])
+
+
+def _time_ms(fn, repeats: int) -> list:
+    """Device time of fn() per repeat (CUDA events on the current stream, one warm-up call)."""
+    fn()
+    out = []
+    for _ in range(repeats):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        out.append(e0.elapsed_time(e1))
+    return out
+
+
+def bench(cfg: EncoderConfig, densities, repeats: int = 3, x=None, weights=None) -> list:
+    """Median sparse-mode encoder time per density against the dense twin (encoder.py:399-436).
+
+    The reference times ``encoder_forward`` on the host; this times the same block engine on the
+    device (CUDA events, one warm-up call per configuration): the sparse encoder at each
+    density and the SAME engine in ``mode="dense"`` (r = keep = 1, encoder.py:416-419) as the
+    dense twin, so ``speedup`` is dense-twin median over sparse median exactly as the reference
+    defines it.  ``x`` defaults to a seeded normal image [H, W, D] (torch generator seeded with
+    cfg.seed + 1, not the reference's splitmix stream); ``weights`` (reference-layout blocks or
+    ``BlockParams``) default to ``weights.random_params(cfg, seed=cfg.seed)`` — the values do not
+    change the timing.  A batch [B, H, W, D] is accepted too.
+    """
+    import dataclasses
+
+    from .weights import random_params
+
+    if repeats < 1:
+        raise ValueError("repeats must be >= 1")
+    dev = _dev()
+    if x is None:
+        g = torch.Generator(device=dev).manual_seed(cfg.seed + 1)
+        xt = torch.randn((cfg.grid.h, cfg.grid.w, cfg.d), generator=g, device=dev)
+    else:
+        xt = _to_dev(x)
+    if xt.dim() == 3:
+        xt = xt[None]
+    if tuple(xt.shape[-3:]) != (cfg.grid.h, cfg.grid.w, cfg.d):
+        raise ValueError(f"input shape {tuple(xt.shape)} != {(cfg.grid.h, cfg.grid.w, cfg.d)}")
+    if weights is None:
+        params = random_params(cfg, dev, seed=cfg.seed)
+    elif isinstance(weights[0], BlockParams):
+        params = list(weights)
+    else:
+        params = params_from_reference(weights, cfg, dev)
+    dense_enc = StripeSortEncoder(cfg, params, dev)
+    dense_ms = _median(_time_ms(lambda: dense_enc(xt, "dense"), repeats))
+    rows = []
+    for density in densities:
+        cfg_r = dataclasses.replace(cfg, r=float(density))
+        enc = StripeSortEncoder(cfg_r, params, dev)
+        med = _median(_time_ms(lambda: enc(xt, "sparse"), repeats))
+        rows.append(BenchRow(density=float(density), achieved_density=cost_report(cfg_r).attn_density(),
+                             median_ms=med, speedup=dense_ms / med))
+    return rows
+
+
+def bench_csv(rows) -> str:
+    """BENCH_COLUMNS table, CRLF line ends, the reference's number formats (encoder.py:439-444)."""
+    lines = [BENCH_COLUMNS]
+    for r in rows:
+        lines.append(f"{r.density!r},{r.achieved_density!r},{r.median_ms:.3f},{r.speedup:.4f}")
+    return "\r\n".join(lines) + "\r\n"
+
+
+def attn_bench(n: int = 4096, d: int = 64, densities=(0.25, 0.5, 1.0), repeats: int = 20, tile: int = 128,
+               seed: int = 0) -> str:
+    """``zstripe attn-bench`` (cli.py:96-130) on the tcgen05 attention kernel: one head of n tokens
+    (a perfect square: the w x w bias grid), identity permutations, tile x tile blocks; median
+    device time per distinct density, speedup against r = 1.0; returns the BENCH_COLUMNS CSV
+    (CRLF).  Inputs are seeded torch normals (bias tables std 0.5, as the reference), staged on the
+    device before timing; head widths d <= 80 run zero-padded to 64 / 80 with tau = 1/sqrt(d)."""
+    w = math.isqrt(n)
+    if w * w != n:
+        raise ValueError(f"--n must be a perfect square for the 2D bias grid, got {n}")
+    densities = [float(r) for r in densities]
+    if not densities:
+        raise ValueError("--densities must name at least one density")
+    if d > 80 or d < 1:
+        raise ValueError(f"head dim {d} outside the B200 kernel's 1..80")
+    dev = _dev()
+    g = torch.Generator(device=dev).manual_seed(seed)
+    dpad = 64 if d <= 64 else 80
+    qkv = [torch.zeros((n, dpad), device=dev, dtype=torch.bfloat16) for _ in range(3)]
+    for t in qkv:
+        t[:, :d] = torch.randn((n, d), generator=g, device=dev).bfloat16()
+    bh = torch.randn((1, n, w), generator=g, device=dev) * 0.5
+    bw = torch.randn((1, n, w), generator=g, device=dev) * 0.5
+    ident = torch.arange(n, device=dev, dtype=torch.int32)
+    out = torch.empty((n, dpad), device=dev, dtype=torch.bfloat16)
+    ws = torch.empty(max(K.attn_ws_bytes(1, 1, n, n, dpad), 256), device=dev, dtype=torch.uint8)
+    t_tiles = -(-n // tile)
+    tau = 1.0 / math.sqrt(d)
+
+    def run(r: float) -> float:
+        prefix = AShapeConfig(b_row=tile, b_col=tile, r=r).prefix_tiles(t_tiles)
+        return _median(_time_ms(lambda: K.stripe_attn(qkv[0], qkv[1], qkv[2], units=1, heads=1, sq=n, sk=n, dh=dpad,
+                                                      bh=bh, bw=bw, q_sp=ident, k_sp=ident, b_row=tile, b_col=tile,
+                                                      prefix=prefix, tau=tau, out=out, ws=ws), repeats))
+
+    medians = {r: run(r) for r in dict.fromkeys(densities)}
+    baseline = medians.get(1.0)
+    if baseline is None:
+        baseline = run(1.0)
+    lines = [BENCH_COLUMNS]
+    for r in densities:
+        lines.append(f"{r!r},{achieved_density(t_tiles, t_tiles, r)!r},{medians[r]:.3f},{baseline / medians[r]:.4f}")
+    return "\r\n".join(lines) + "\r\n"

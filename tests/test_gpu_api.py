@@ -145,3 +145,31 @@ def test_global_attention_vs_reference_golden(ci):
     got = api.ashape_attention(q, k, v, api.BiasTables(bh, bw), sp, sp, Z.AShapeConfig(b_row=128, b_col=128, r=r))
     rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     assert rel <= 1e-2 and np.abs(got - ref).max() <= 3e-2, (rel, np.abs(got - ref).max())
+
+
+@pytest.mark.gpu
+def test_bench_schema_matches_reference():
+    """api.bench / bench_csv / attn_bench: the reference's columns, number formats and speedup
+    definition (encoder.py:388-444, cli.py:96-130), timed on the device."""
+    import re
+
+    from paper_2605_17633_b200 import api
+    from paper_2605_17633_b200.config import EncoderConfig, GridShape
+
+    cfg = EncoderConfig(grid=GridShape(64, 64), d=768, heads=12, window=14, layout=("local", "global"), r=0.4,
+                        keep_fraction=0.4, seed=3)
+    rows = api.bench(cfg, [0.25, 1.0], repeats=2)
+    assert [r.density for r in rows] == [0.25, 1.0]
+    assert all(r.median_ms > 0 and r.speedup > 0 for r in rows)
+    assert rows[1].achieved_density == 1.0
+    assert rows[0].achieved_density == api.cost_report(__import__("dataclasses").replace(cfg, r=0.25)).attn_density()
+    csv = api.bench_csv(rows)
+    lines = csv.split("\r\n")
+    assert lines[0] == api.BENCH_COLUMNS == "density,achieved_density,median_ms,speedup" and lines[-1] == ""
+    assert re.fullmatch(r"0\.25,[0-9.e-]+,\d+\.\d{3},\d+\.\d{4}", lines[1])
+    ab = api.attn_bench(n=1024, d=64, densities=(0.25, 0.5, 0.25), repeats=3, tile=128)
+    al = ab.split("\r\n")
+    assert al[0] == api.BENCH_COLUMNS and len(al) == 5 and al[-1] == ""
+    assert al[1].startswith("0.25,0.") and al[3].startswith("0.25,")
+    with pytest.raises(ValueError):
+        api.attn_bench(n=1000)

@@ -104,3 +104,13 @@ def test_shard_bounds_partition():
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             assert max(shard_counts(n, world)) - min(shard_counts(n, world)) <= 1
     assert shard_counts(64, 8) == [8] * 8
+
+
+def test_bench_csv_bytes_match_reference():
+    """api.bench_csv writes the reference's bytes (encoder.py:439-444); the expected string is the
+    output of the reference's own bench_csv on these rows (generated with zstripe.encoder)."""
+    from paper_2605_17633_b200 import api
+
+    rows = [api.BenchRow(0.25, 0.3125, 1.23456, 2.5), api.BenchRow(1.0, 1.0, 10.0, 1.0)]
+    assert api.bench_csv(rows) == ("density,achieved_density,median_ms,speedup\r\n0.25,0.3125,1.235,2.5000\r\n"
+                                   "1.0,1.0,10.000,1.0000\r\n")
