@@ -427,11 +427,12 @@ def encoder_forward(x, weights, cfg: EncoderConfig, mode: str = "sparse"):
     blocks) or already-converted ``BlockParams``.  ``CostReport.ms`` holds each
     block's device time (CUDA events around its launches).
 
-    Shape envelope of the B200 block engine: head dim d / heads must be 64 or 80
-    and d a multiple of 64 (the SAM ViT-B/L/H widths); other widths, e.g. the
-    reference's toy default d = 64 with 4 heads (dh = 16), raise ValueError.  The
-    per-op entry points (``ashape_attention``, ``route_mlp``) zero-pad heads up to
-    80 and take any width.
+    Shape envelope of the B200 block engine: d a multiple of 64 and head dim
+    d / heads <= 80; heads narrower than 64 (e.g. the reference's default d = 64
+    with 4 heads, dh = 16) run zero-padded to 64 columns with tau = 1/sqrt(dh)
+    (``encoder._pad_heads``), other widths raise ValueError.  The per-op entry
+    points (``ashape_attention``, ``route_mlp``) zero-pad heads up to 80 and take
+    any width.
     """
     if mode not in ("dense", "sparse"):
         raise ValueError(f"mode must be 'dense' or 'sparse', got {mode!r}")

@@ -72,6 +72,27 @@ class Orderings:
     maps: dict
 
 
+def _pad_heads(blk: BlockParams, H: int, dh: int, dp: int) -> BlockParams:
+    """``blk`` with every head widened from dh to dp columns (zeros): QKV weight rows / bias of
+    Q, K and V, the proj weight's input columns and SAM rel-pos tables."""
+    import dataclasses
+
+    C = blk.qkv_w.shape[1]
+    idx = (torch.arange(H, device=blk.qkv_w.device)[:, None] * dp + torch.arange(dh, device=blk.qkv_w.device)).reshape(-1)
+    qkv_w = blk.qkv_w.new_zeros((3 * H * dp, C))
+    qkv_b = blk.qkv_b.new_zeros(3 * H * dp)
+    for part in range(3):
+        qkv_w[part * H * dp + idx] = blk.qkv_w[part * H * dh:(part + 1) * H * dh]
+        qkv_b[part * H * dp + idx] = blk.qkv_b[part * H * dh:(part + 1) * H * dh]
+    proj_w = blk.proj_w.new_zeros((blk.proj_w.shape[0], H * dp))
+    proj_w[:, idx] = blk.proj_w
+    extra = {}
+    if blk.rel_pos_h is not None:
+        extra = dict(rel_pos_h=torch.nn.functional.pad(blk.rel_pos_h, (0, dp - dh)),
+                     rel_pos_w=torch.nn.functional.pad(blk.rel_pos_w, (0, dp - dh)))
+    return dataclasses.replace(blk, qkv_w=qkv_w, qkv_b=qkv_b, proj_w=proj_w, **extra)
+
+
 class StripeSortEncoder:
     """Runs the SparseSAM block stack on a batch of fp32 token grids ``[B, H, W, C]``.
 
@@ -84,12 +105,20 @@ class StripeSortEncoder:
         if len(params) != len(cfg.layout):
             raise ValueError(f"{len(params)} weight sets for {len(cfg.layout)} blocks")
         hd = cfg.head_dim
-        if hd not in (64, 80):
-            raise ValueError(f"head dim {hd} unsupported by the B200 attention kernel (64 or 80)")
+        if hd > 80:
+            raise ValueError(f"head dim {hd} > 80 unsupported by the B200 attention kernel")
         if cfg.d % 64:
             raise ValueError("model width must be a multiple of 64 for the tcgen05 GEMMs")
+        # heads narrower than the attention kernel's 64 / 80 run zero-padded: Q / K / V columns
+        # [h * dp + dh, (h + 1) * dp) are zero (zero QKV weight rows and bias), the proj weight has
+        # zero input columns there, tau stays 1 / sqrt(dh) — the same math as the unpadded heads
+        self.dh = hd
+        self.dp = 64 if hd <= 64 else 80
+        self.Cq = cfg.heads * self.dp
+        if self.Cq % 64:
+            raise ValueError(f"{cfg.heads} heads of {self.dp} (padded) columns: width not a multiple of 64")
         self.cfg = cfg
-        self.params = params
+        self.params = params if self.dp == hd else [_pad_heads(b, cfg.heads, hd, self.dp) for b in params]
         self.device = torch.device(device)
         g = cfg.grid
         self.HW = g.n()
@@ -130,8 +159,8 @@ class StripeSortEncoder:
             xa=torch.empty((R, C), device=dev, dtype=torch.float32),
             xb=torch.empty((R, C), device=dev, dtype=torch.float32),
             h=torch.empty((R, C), device=dev, dtype=torch.bfloat16),
-            qkv=torch.empty((R, 3 * C), device=dev, dtype=torch.bfloat16),
-            o=torch.empty((R, C), device=dev, dtype=torch.bfloat16),
+            qkv=torch.empty((R, 3 * self.Cq), device=dev, dtype=torch.bfloat16),
+            o=torch.empty((R, self.Cq), device=dev, dtype=torch.bfloat16),
             mlp=torch.empty((0,), device=dev, dtype=torch.bfloat16),
         )
         self._ws, self._ws_B = ws, B
@@ -199,7 +228,7 @@ class StripeSortEncoder:
     def _block(self, blk: BlockParams, x: torch.Tensor, od: Orderings, B: int, r: float, rows: dict,
                ws: dict, nonpad: dict | None = None) -> None:
         cfg = self.cfg
-        C, H, dh = cfg.d, cfg.heads, cfg.head_dim
+        C, H, dh, dp, Cq = cfg.d, cfg.heads, self.dh, self.dp, self.Cq
         local = blk.kind == "local"
         S = self.S2 if local else self.HW
         U = B * self.nwin if local else B
@@ -223,10 +252,10 @@ class StripeSortEncoder:
                 qkv = K.gemm(h, blk.qkv_w, blk.qkv_b, out=ws["qkv"][:R], row_map=npr, m_dev=nn)
                 # K and V columns only: pad tokens are keys / values of the window, but their own
                 # query rows are dropped (o_rows), so their Q part is never needed
-                K.fill_flagged_rows(qkv[:, C:], self._pad_qkv_row(blk)[0, C:], od.maps["l_is_pad"])
+                K.fill_flagged_rows(qkv[:, Cq:], self._pad_qkv_row(blk)[0, Cq:], od.maps["l_is_pad"])
             with tr.span(f"attn_{blk.kind}", flops=4.0 * dh * E * U * H,
                          bytes=U * H * 4 * S * dh * 2 + H * 2 * S * w * 4):
-                o = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], units=U, heads=H, sq=S, sk=S, dh=dh,
+                o = K.stripe_attn(qkv[:, :Cq], qkv[:, Cq:2 * Cq], qkv[:, 2 * Cq:], units=U, heads=H, sq=S, sk=S, dh=dp,
                                   q_sp=sig, k_sp=sig, b_row=tile, b_col=tile, prefix=prefix,
                                   tau=1.0 / math.sqrt(dh), out=ws["o"][:R], o_rows=nonpad["omap"], **bias)
             with tr.span("gemm_proj", flops=(nn, 2.0 * C * C)):
@@ -238,7 +267,7 @@ class StripeSortEncoder:
                 qkv = K.gemm(h, blk.qkv_w, blk.qkv_b, out=ws["qkv"][:R])
             with tr.span(f"attn_{blk.kind}", flops=4.0 * dh * E * U * H,
                          bytes=U * H * 4 * S * dh * 2 + H * 2 * S * w * 4):
-                o = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], units=U, heads=H, sq=S, sk=S, dh=dh,
+                o = K.stripe_attn(qkv[:, :Cq], qkv[:, Cq:2 * Cq], qkv[:, 2 * Cq:], units=U, heads=H, sq=S, sk=S, dh=dp,
                                   q_sp=sig, k_sp=sig, b_row=tile, b_col=tile, prefix=prefix,
                                   tau=1.0 / math.sqrt(dh), out=ws["o"][:R], **bias)
             with tr.span("gemm_proj", flops=2.0 * R * C * C, bytes=R * C * 2 + C * C * 2 + R * C * 8):

@@ -256,3 +256,16 @@ def test_launch_count_matches_profiler():
     ours = [e for e in kern if "at::" not in e.name]  # PyTorch's own kernels live in namespace at::
     assert n == len(ours), (n, len(ours), sorted({e.name[:60] for e in kern})[:30])
     assert n > 100  # ViT-B: orderings, 12 blocks x ~9 launches, frame
+
+
+@pytest.mark.parametrize("hw", [28, 20])
+def test_reference_default_config_padded_heads(hw):
+    """The reference's default EncoderConfig (d = 64, 4 heads of 16, window 14, local-local-global,
+    r = 0.25, keep 0.5; encoder.py:46-58) runs on the block engine with heads zero-padded to 64
+    columns (encoder._pad_heads) and matches the oracle; 20x20 adds padded windows."""
+    ocfg = O.EncCfg(h=hw, w=hw, d=64, heads=4, window=14, layout=("local", "local", "global"), r=(0.25,) * 3,
+                    keep=(0.5,) * 3, seed=0)
+    x = O.SplitMix(11).normal((hw, hw, 64))
+    w = O.init_weights(ocfg)
+    y, _ = api.encoder_forward(x, w, _oracle_to_ref_cfg(ocfg))
+    assert_close(y, O.encoder_forward(x, w, ocfg), f"default config {hw}x{hw}")
