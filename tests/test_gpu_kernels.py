@@ -233,7 +233,10 @@ def _attn_case(units, heads, S, dh, w, tile, r, seed=0, bscale=0.5, stripes=Fals
     qkv = torch.randn(units * S, 3 * C, generator=g).bfloat16().to(DEV)
     bh = (bscale * torch.randn(heads, S, w, generator=g)).to(DEV)
     bw = (bscale * torch.randn(heads, S, w, generator=g)).to(DEV)
-    mk = (lambda: _parity_stripes(S, w, g)) if stripes else (lambda: torch.randperm(S, generator=g))
+    if stripes == "shifted":  # class boundaries mid-chunk: parity-pure and mixed chunks in one item
+        mk = lambda: torch.roll(_parity_stripes(S, w, g), 64)  # noqa: E731
+    else:
+        mk = (lambda: _parity_stripes(S, w, g)) if stripes else (lambda: torch.randperm(S, generator=g))
     sp = torch.stack([mk() for _ in range(units)]).int().to(DEV)
     T = -(-S // tile)
     out = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], units=units, heads=heads, sq=S, sk=S, dh=dh,
@@ -298,6 +301,7 @@ def test_attention_global_parity_stripes(dh, r):
     (y % 2, x % 2) class), 4096- and 1024-token grids."""
     assert _attn_case(2, 2, 4096, dh, 64, 128, r, seed=8, stripes=True) < 1e-2
     assert _attn_case(3, 2, 1024, dh, 32, 128, r, seed=9, stripes=True) < 1e-2
+    assert _attn_case(2, 2, 4096, dh, 64, 128, r, seed=10, stripes="shifted") < 1e-2
 
 
 @pytest.mark.parametrize("S,w,tile", [(4096, 64, 128), (196, 14, 32)])
