@@ -449,8 +449,7 @@ def encoder_forward(x, weights, cfg: EncoderConfig, mode: str = "sparse"):
     if single:
         xt = xt[None]
     # per-block device time from CUDA events around each block's launches (the reference's
-    # per-block wall clock, encoder.py:342,372; the first block also carries the layout switch
-    # out of the spatial order, the orderings and final permute are outside every block)
+    # per-block wall clock, encoder.py:342,372; the orderings are outside every block)
     enc.block_events = []
     y = enc(xt, mode)
     torch.cuda.synchronize()

@@ -134,7 +134,7 @@ class StripeSortEncoder:
         self.has_local = "local" in cfg.layout
         self.has_global = "global" in cfg.layout
         self.tracer = NULL
-        # list -> (start, end) CUDA events of every block are appended to it (layout switch included)
+        # list -> (start, end) CUDA events of every block are appended to it
         self.block_events: list | None = None
 
     # ------------------------------------------------------------ workspace
@@ -156,8 +156,6 @@ class StripeSortEncoder:
         RG = B * self.HW
         R = max(RL, RG)
         ws = dict(
-            xa=torch.empty((R, C), device=dev, dtype=torch.float32),
-            xb=torch.empty((R, C), device=dev, dtype=torch.float32),
             h=torch.empty((R, C), device=dev, dtype=torch.bfloat16),
             qkv=torch.empty((R, 3 * self.Cq), device=dev, dtype=torch.bfloat16),
             o=torch.empty((R, self.Cq), device=dev, dtype=torch.bfloat16),
@@ -209,6 +207,22 @@ class StripeSortEncoder:
             rows, offs = K.unit_span_rows(U, S, 0, S, od.maps["l_is_pad"], self.device)
             sets["nonpad"] = dict(rows=rows, n=offs[U:U + 1], max=U * S,
                                   omap=K.invert_rows(rows, U * S, n_dev=offs[U:U + 1]))
+        # the residual stream stays in spatial row order for the whole forward: every row set of a
+        # block's scan order is composed with that order's spatial row map (slots past the device
+        # count hold unused garbage: clamped, never read by the kernels)
+        m = od.maps
+
+        def to_spatial(rows_, kind):
+            mp = m["l_from_s"] if kind == "local" else m["g_from_s"]
+            return mp[rows_.clamp(0, mp.numel() - 1).long()]
+
+        for key, e in sets.items():
+            if key == "nonpad":
+                e["rows_s"] = to_spatial(e["rows"], "local")
+                continue
+            e["keep_s"] = to_spatial(e["keep"], key[0])
+            if "bypass" in e:
+                e["bypass_s"] = to_spatial(e["bypass"], key[0])
         return sets
 
     def _pad_qkv_row(self, blk: BlockParams) -> torch.Tensor:
@@ -237,7 +251,7 @@ class StripeSortEncoder:
         T = -(-S // tile)
         prefix = math.floor(r * T)
         sig = od.sigma_loc if local else od.sigma_glob
-        xs = x[:R]
+        xs = x  # the spatial residual rows (every access goes through a row map)
         tr = self.tracer
         w = blk.side
         E = attention_elements(S, tile, prefix)
@@ -245,9 +259,9 @@ class StripeSortEncoder:
                 else dict(bh=blk.bh, bw=blk.bw))
         if nonpad is not None:
             # non-pad rows only (compacted), pad K/V rows = the constant row of LN(0) = beta
-            npr, nn, mx = nonpad["rows"], nonpad["n"], nonpad["max"]
+            npr, nps, nn, mx = nonpad["rows"], nonpad["rows_s"], nonpad["n"], nonpad["max"]
             with tr.span("layernorm", bytes=(nn, C * 6)):
-                h = K.layernorm_rows(xs, blk.ln1_g, blk.ln1_b, npr, out=ws["h"][:mx], n_dev=nn)
+                h = K.layernorm_rows(xs, blk.ln1_g, blk.ln1_b, nps, out=ws["h"][:mx], n_dev=nn)
             with tr.span("gemm_qkv", flops=(nn, 2.0 * C * 3 * C)):
                 qkv = K.gemm(h, blk.qkv_w, blk.qkv_b, out=ws["qkv"][:R], row_map=npr, m_dev=nn)
                 # K and V columns only: pad tokens are keys / values of the window, but their own
@@ -259,10 +273,11 @@ class StripeSortEncoder:
                                   q_sp=sig, k_sp=sig, b_row=tile, b_col=tile, prefix=prefix,
                                   tau=1.0 / math.sqrt(dh), out=ws["o"][:R], o_rows=nonpad["omap"], **bias)
             with tr.span("gemm_proj", flops=(nn, 2.0 * C * C)):
-                K.gemm(o[:mx], blk.proj_w, blk.proj_b, epi=K.EPI_F32_RESID, out=xs, res=xs, row_map=npr, m_dev=nn)
+                K.gemm(o[:mx], blk.proj_w, blk.proj_b, epi=K.EPI_F32_RESID, out=xs, res=xs, row_map=nps, m_dev=nn)
         else:
+            g2s = od.maps["g_from_s"] if not local else od.maps["l_from_s"]  # scan-order row -> spatial row
             with tr.span("layernorm", bytes=R * C * 6):
-                h = K.layernorm_rows(xs, blk.ln1_g, blk.ln1_b, out=ws["h"][:R])
+                h = K.layernorm_rows(xs, blk.ln1_g, blk.ln1_b, g2s, out=ws["h"][:R])
             with tr.span("gemm_qkv", flops=2.0 * R * C * 3 * C, bytes=R * C * 2 + 3 * C * C * 2 + R * 3 * C * 2):
                 qkv = K.gemm(h, blk.qkv_w, blk.qkv_b, out=ws["qkv"][:R])
             with tr.span(f"attn_{blk.kind}", flops=4.0 * dh * E * U * H,
@@ -271,8 +286,7 @@ class StripeSortEncoder:
                                   q_sp=sig, k_sp=sig, b_row=tile, b_col=tile, prefix=prefix,
                                   tau=1.0 / math.sqrt(dh), out=ws["o"][:R], **bias)
             with tr.span("gemm_proj", flops=2.0 * R * C * C, bytes=R * C * 2 + C * C * 2 + R * C * 8):
-                K.gemm(o, blk.proj_w, blk.proj_b, epi=K.EPI_F32_RESID, out=xs, res=xs,
-                       zero_rows=od.maps["l_is_pad"] if local else None)
+                K.gemm(o, blk.proj_w, blk.proj_b, epi=K.EPI_F32_RESID, out=xs, res=xs, row_map=g2s)
         # RC-MLP (mlp.py:88-114): gather-LN of the kept rows -> fc1 + GELU -> fc2 + scatter-add residual
         nk = rows["n_keep"]
         mk = rows["max_keep"]
@@ -280,15 +294,15 @@ class StripeSortEncoder:
         hln = ws["mlp"][: mk * C].view(mk, C)
         hid = ws["mlp"][mk * C: mk * (C + hidden)].view(mk, hidden)
         with tr.span("mlp_ln", bytes=(nk, C * 6)):
-            K.layernorm_rows(xs, blk.ln2_g, blk.ln2_b, rows["keep"], out=hln, n_dev=nk)
+            K.layernorm_rows(xs, blk.ln2_g, blk.ln2_b, rows["keep_s"], out=hln, n_dev=nk)
         with tr.span("gemm_fc1", flops=(nk, 2.0 * C * hidden)):
             K.gemm(hln, blk.w1, blk.b1, epi=K.EPI_BF16_GELU, out=hid, m_dev=nk)
         with tr.span("gemm_fc2", flops=(nk, 2.0 * C * hidden)):
-            K.gemm(hid, blk.w2, blk.b2, epi=K.EPI_F32_RESID, out=xs, res=xs, row_map=rows["keep"], m_dev=nk)
+            K.gemm(hid, blk.w2, blk.b2, epi=K.EPI_F32_RESID, out=xs, res=xs, row_map=rows["keep_s"], m_dev=nk)
         if "bypass" in rows:
             with tr.span("mlp_ln", bytes=(rows["n_bypass"], C * 8)):
-                K.layernorm_rows(xs, blk.ln2_g, blk.ln2_b, rows["bypass"], out_f32=True, out=xs,
-                                 out_rows=rows["bypass"], n_dev=rows["n_bypass"])
+                K.layernorm_rows(xs, blk.ln2_g, blk.ln2_b, rows["bypass_s"], out_f32=True, out=xs,
+                                 out_rows=rows["bypass_s"], n_dev=rows["n_bypass"])
 
     def forward_rows(self, x0: torch.Tensor, mode: str = "sparse", orderings: Orderings | None = None,
                      out: torch.Tensor | None = None) -> torch.Tensor:
@@ -308,36 +322,27 @@ class StripeSortEncoder:
                 orderings = self.orderings(x0)
         od = orderings
         rows = self._row_sets(B, od, mode)
-        m = od.maps
         flat = x0.reshape(B * self.HW, cfg.d)
-        cur, spare = ws["xa"], ws["xb"]
-        layout = None
+        # the residual stream lives in spatial row order in `out` for the whole forward (every
+        # block reads and writes it through its scan order's row maps: no layout permutes);
+        # out may be x0 itself (in place, after the orderings were taken from it)
+        if out is None:
+            out = torch.empty((B * self.HW, cfg.d), device=self.device, dtype=torch.float32)
+        if out.data_ptr() != flat.data_ptr():
+            out.copy_(flat)
         for bi, blk in enumerate(self.params):
             kind = blk.kind
             if self.block_events is not None:  # per-block device time (CostReport.ms, encoder.py:342,372)
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                 ev[0].record()
                 self.block_events.append(ev)
-            if kind != layout:
-                if layout is None:
-                    src, mp = flat, (m["l_from_s"] if kind == "local" else m["g_from_s"])
-                else:
-                    src, mp = cur, (m["l_from_g"] if kind == "local" else m["g_from_l"])
-                with self.tracer.span("permute", bytes=mp.numel() * cfg.d * 8):
-                    K.permute_rows(src, mp, out=spare[: mp.numel()])
-                cur, spare = spare, cur
-                layout = kind
             r = 1.0 if mode == "dense" else cfg.r[bi]
             kf = 1.0 if mode == "dense" else cfg.keep_fraction[bi]
             S = self.S2 if kind == "local" else self.HW
             Kc = RouterConfig(kf, cfg.bypass_mode).keep_count(S)
-            self._block(blk, cur, od, B, r, rows[(kind, Kc)], ws, rows.get("nonpad") if kind == "local" else None)
+            self._block(blk, out, od, B, r, rows[(kind, Kc)], ws, rows.get("nonpad") if kind == "local" else None)
             if self.block_events is not None:
                 self.block_events[-1][1].record()
-        if out is None:
-            out = torch.empty((B * self.HW, cfg.d), device=self.device, dtype=torch.float32)
-        with self.tracer.span("permute", bytes=out.numel() * 8):
-            K.permute_rows(cur, m["s_from_l"] if layout == "local" else m["s_from_g"], out=out)
         return out
 
     def __call__(self, x0: torch.Tensor, mode: str = "sparse") -> torch.Tensor:
@@ -380,7 +385,6 @@ class SparseSAMImageEncoder:
             C, HW, dev = self.cfg.d, self.cfg.grid.n(), self.device
             self._bufs_d = dict(
                 x0=torch.empty((B * HW, C), device=dev, dtype=torch.float32),
-                xo=torch.empty((B * HW, C), device=dev, dtype=torch.float32),
                 xb16=torch.empty((B * HW, C), device=dev, dtype=torch.bfloat16),
                 n1=torch.empty((B * HW, SAM_NECK), device=dev, dtype=torch.float32),
                 n1b=torch.empty((B * HW, SAM_NECK), device=dev, dtype=torch.bfloat16),
@@ -421,7 +425,7 @@ class SparseSAMImageEncoder:
         B = img.shape[0]
         g = self.cfg.grid
         x0 = self.embed(img)
-        xo = self.core.forward_rows(x0.view(B, g.h, g.w, self.cfg.d), mode, out=self._bufs(B)["xo"])
+        xo = self.core.forward_rows(x0.view(B, g.h, g.w, self.cfg.d), mode, out=x0)  # in place
         return self.neck(xo, B, out=out)
 
 
