@@ -205,16 +205,53 @@ def run_reference(args):
 
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clock + throttle reasons sampled DURING the timed region.
+
+    In-process NVML (nvidia-ml-py) from a background thread every 5 ms, so even a timed region of
+    a few milliseconds (ViT-B, one image) gets samples; falls back to `nvidia-smi -lms 100`."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+
     def __init__(self, idx: int):
-        self.path = tempfile.mktemp(suffix=".csv")
-        self.proc = None
         self.idx = idx
+        self.rows = []  # (sm_mhz, reason bitmask)
+        self.max_mhz = None
+        self.nvml = None
+        self.proc = None
+        self.path = None
 
     def __enter__(self):
+        import threading
+
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = self._nvml_handle(N)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+            self.nvml, self._h = N, h
+            self._stop = threading.Event()
+
+            def run():
+                while True:
+                    try:
+                        self.rows.append((float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)),
+                                          int(N.nvmlDeviceGetCurrentClocksEventReasons(h))))
+                    except Exception:  # noqa: BLE001
+                        pass
+                    if self._stop.wait(0.005):
+                        return
+
+            self._thr = threading.Thread(target=run, daemon=True)
+            self._thr.start()
+            return self
+        except Exception:  # noqa: BLE001
+            self.nvml = None
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
+            self.path = tempfile.mktemp(suffix=".csv")
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -223,7 +260,27 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def _nvml_handle(self, N):
+        """NVML handle of CUDA device `idx` (matched by PCI location: CUDA_VISIBLE_DEVICES may
+        renumber devices, NVML indices never are)."""
+        try:
+            import torch
+
+            pr = torch.cuda.get_device_properties(self.idx)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return N.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:  # noqa: BLE001
+            return N.nvmlDeviceGetHandleByIndex(self.idx)
+
     def __exit__(self, *exc):
+        if self.nvml is not None:
+            self._stop.set()
+            self._thr.join(timeout=2)
+            try:  # one last sample: the region ended just now
+                self.rows.append((float(self.nvml.nvmlDeviceGetClockInfo(self._h, self.nvml.NVML_CLOCK_SM)),
+                                  int(self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self._h))))
+            except Exception:  # noqa: BLE001
+                pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -233,6 +290,13 @@ class ClockSampler:
             self.f.close()
 
     def summary(self) -> dict:
+        if self.nvml is not None:
+            if not self.rows:
+                return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "source": "nvml"}
+            sm = sorted(r[0] for r in self.rows)
+            reasons = sorted({n for _, m in self.rows for n, bit in self.REASONS.items() if m & bit})
+            return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                    "samples": len(self.rows), "source": "nvml, 5 ms"}
         try:
             rows = [r.split(", ") for r in Path(self.path).read_text().strip().splitlines() if r.strip()]
         except Exception:  # noqa: BLE001
@@ -242,7 +306,8 @@ class ClockSampler:
         sm = sorted(float(r[1]) for r in rows)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.strip() == "Active"})
-        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][2]), "reasons": reasons, "samples": len(rows)}
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][2]), "reasons": reasons, "samples": len(rows),
+                "source": "nvidia-smi, 100 ms"}
 
 
 # --------------------------------------------------------------------------- multi-rank helpers
