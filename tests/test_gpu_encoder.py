@@ -269,3 +269,16 @@ def test_reference_default_config_padded_heads(hw):
     w = O.init_weights(ocfg)
     y, _ = api.encoder_forward(x, w, _oracle_to_ref_cfg(ocfg))
     assert_close(y, O.encoder_forward(x, w, ocfg), f"default config {hw}x{hw}")
+
+
+def test_encoder_layernorm_bypass_vs_oracle():
+    """bypass_mode="layernorm" (mlp.py:99-114: routed-out rows get LN instead of identity) through
+    the block engine, whose bypass rows are scattered into the spatial residual by row map."""
+    ocfg = O.EncCfg(h=20, w=20, d=128, heads=2, window=6, layout=("local", "global", "local"), r=(0.4,) * 3,
+                    keep=(0.5,) * 3, seed=7, bypass="layernorm")
+    x = O.SplitMix(12).normal((20, 20, 128))
+    w = O.init_weights(ocfg)
+    cfg = Z.EncoderConfig(grid=Z.GridShape(20, 20), d=128, heads=2, window=6, layout=ocfg.layout, r=ocfg.r,
+                          keep_fraction=ocfg.keep, seed=7, bypass_mode="layernorm")
+    y, _ = api.encoder_forward(x, w, cfg)
+    assert_close(y, O.encoder_forward(x, w, ocfg), "layernorm bypass")
