@@ -370,34 +370,6 @@ __device__ __forceinline__ uint32_t exp2_pair_bf16_ns(float s0, float s1, unsign
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(e1), "f"(e0));
   return p;
 }
-// exp2_pair_bf16_ns on the FMA / ALU pipes (no MUFU): t = s * c + m2 (FFMA2), clamped at -127,
-// split t = n + f with n = round(t) (magic-number add, FADD2) and f in [-0.5, 0.5], 2^f by a
-// degree-3 polynomial with p(0) = 1 (Lawson minimax on [-0.5, 0.5], max relative error 1.0e-4,
-// below the bf16 rounding of P: 2^-9), 2^n added to the exponent as an integer.  t = -inf or
-// NaN gives 0.  Used for a fixed share of the softmax pairs so the exponentials of one warp
-// overlap on two pipes (the MUFU alone issues one warp instruction per 8 cycles per SMSP).
-__device__ __forceinline__ uint32_t exp2_pair_bf16_poly(float s0, float s1, unsigned long long c2,
-                                                        unsigned long long m2) {
-  unsigned long long t, r, n, f, p;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(t) : "l"(f32x2(s0, s1)), "l"(c2), "l"(m2));
-  float2 tt = unpack_f32x2(t);
-  tt.x = fmaxf(tt.x, -127.f);
-  tt.y = fmaxf(tt.y, -127.f);
-  t = f32x2(tt.x, tt.y);
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(t), "l"(f32x2(12582912.f, 12582912.f)));   // 1.5 * 2^23
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(n) : "l"(r), "l"(f32x2(-12582912.f, -12582912.f)));  // round(t)
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(f) : "l"(n), "l"(f32x2(-1.f, -1.f)), "l"(t));    // t - n
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(f32x2(0.05500893f, 0.05500893f)), "l"(f),
-      "l"(f32x2(0.24221098f, 0.24221098f)));
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(p), "l"(f), "l"(f32x2(0.6932829f, 0.6932829f)));
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p) : "l"(p), "l"(f), "l"(f32x2(1.f, 1.f)));
-  const float2 pp = unpack_f32x2(p), rr = unpack_f32x2(r);
-  const float e0 = __uint_as_float(__float_as_uint(pp.x) + (__float_as_uint(rr.x) << 23));
-  const float e1 = __uint_as_float(__float_as_uint(pp.y) + (__float_as_uint(rr.y) << 23));
-  uint32_t o;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(o) : "f"(e1), "f"(e0));
-  return o;
-}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
