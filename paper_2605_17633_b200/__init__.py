@@ -3,8 +3,9 @@
 Drop-in for the reference ``zstripe`` package's hot path (stripe-sort
 attention, residual-consistency MLP, saliency ordering, Z-order permutation):
 the same functional API (``api``), configuration types (``config``), the
-batched device engine (``encoder.StripeSortEncoder``) and the SAM image
-encoder frame (``encoder.SparseSAMImageEncoder``).  All compute runs in the
+batched device engine (``encoder.StripeSortEncoder``), the SAM image
+encoder frame (``encoder.SparseSAMImageEncoder``) and PyTorch modules with
+segment_anything's image-encoder parameter tree (``modules``).  All compute runs in the
 hand-written kernels of ``_lib/libzstripe_b200.so``; there is no CPU fallback.
 """
 

@@ -114,3 +114,21 @@ def test_bench_csv_bytes_match_reference():
     rows = [api.BenchRow(0.25, 0.3125, 1.23456, 2.5), api.BenchRow(1.0, 1.0, 10.0, 1.0)]
     assert api.bench_csv(rows) == ("density,achieved_density,median_ms,speedup\r\n0.25,0.3125,1.235,2.5000\r\n"
                                    "1.0,1.0,10.000,1.0000\r\n")
+
+
+def test_module_api_mirrors_sam_parameter_tree():
+    """modules.SparseSAMImageEncoderViT has SAM ImageEncoderViT's parameter names and shapes (ViT-B
+    constructor arguments of segment_anything build_sam_vit_b), so SAM state_dicts load."""
+    from paper_2605_17633_b200 import modules as M
+
+    enc = M.SparseSAMImageEncoderViT(depth=12, embed_dim=768, img_size=1024, mlp_ratio=4, num_heads=12,
+                                     qkv_bias=True, use_rel_pos=True, global_attn_indexes=(2, 5, 8, 11),
+                                     window_size=14, out_chans=256)
+    sd = enc.state_dict()
+    assert sd["patch_embed.proj.weight"].shape == (768, 3, 16, 16) and sd["pos_embed"].shape == (1, 64, 64, 768)
+    assert sd["blocks.0.attn.qkv.weight"].shape == (2304, 768) and sd["blocks.0.attn.rel_pos_h"].shape == (27, 64)
+    assert sd["blocks.2.attn.rel_pos_w"].shape == (127, 64) and sd["blocks.3.mlp.lin1.weight"].shape == (3072, 768)
+    assert sd["neck.0.weight"].shape == (256, 768, 1, 1) and sd["neck.2.weight"].shape == (256, 256, 3, 3)
+    assert sd["neck.3.bias"].shape == (256,)
+    assert [b.kind for b in enc.blocks].count("global") == 4
+    assert len(sd) == 3 + 12 * 14 + 6  # SAM vit_b image encoder: 177 entries
