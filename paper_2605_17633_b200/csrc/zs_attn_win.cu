@@ -53,6 +53,7 @@ struct Params {
   const int* k_sp;
   float tau;
   int rb;       // rows of the tile-B operands (ceil16(S-128)), 0 when nt == 1
+  int seq;      // 1: tiles A and B share the S columns and run one after the other (dense-ish windows)
   int kv_rows;  // rows of the K/V slabs
   // smem layout (byte offsets from the 1024-aligned base; buffer b adds b * buf_bytes)
   int off_qa, off_k, off_qb, off_v, off_qa_t, off_k_t, off_qb_t, off_v_t, buf_bytes;
@@ -346,7 +347,30 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         umma_commit_elect(&o_full[X]);
       };
       int k = 0, pb = 0;
-      for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
+      if (P.seq) {
+        // high densities (S_A + S_B + 2 O > 512 columns): the two tiles share the S columns and run
+        // back to back — S_A, PV_A, S_B (issued after PV_A: in-order, so P_A is read before S_B
+        // overwrites it), PV_B — with Q / K / V of the next item still double-buffered
+        for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
+          const int b = k & 1;
+          mbar_wait(&qk_full[b], (k >> 1) & 1);
+          mbar_wait(bk_full, k & 1);
+          tc_fence_after();
+          issue_s(0, b);
+          mbar_wait_sleep(&p_full[0], k & 1);
+          mbar_wait(&v_full[b], (k >> 1) & 1);
+          tc_fence_after();
+          issue_pv(0, b);
+          issue_s(1, b);
+          umma_commit_elect(&qk_empty[b]);
+          umma_commit_elect(bk_empty);
+          mbar_wait_sleep(&p_full[1], k & 1);
+          tc_fence_after();
+          issue_pv(1, b);
+          umma_commit_elect(&v_empty[b]);
+        }
+      }
+      for (int it = P.seq ? P.items : blockIdx.x; it < P.items; it += gridDim.x, ++k) {
         const int b = k & 1;
         mbar_wait(&qk_full[b], (k >> 1) & 1);
         mbar_wait(bk_full, k & 1);
@@ -374,7 +398,7 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         if (nt == 1) umma_commit_elect(&v_empty[b]);
         pb = b;
       }
-      if (nt > 1 && k > 0) {
+      if (nt > 1 && k > 0 && !P.seq) {
         mbar_wait(&p_full[1], (k - 1) & 1);
         tc_fence_after();
         issue_pv(1, pb);
@@ -667,10 +691,16 @@ int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, 
     p.s_col[X] = col;  // width for now
   }
   const int wa = (p.s_col[0] + 31) & ~31, wb = p.s_col[1];
-  if (wa + wb + 2 * 80 > (int)kTmemCols) return 1;  // dense (r = 1) windows: generic kernel
+  p.seq = 0;
+  if (wa + wb + 2 * 80 > (int)kTmemCols) {
+    // high density: tiles A and B one after the other over shared S columns
+    if (p.nt < 2 || std::max(wa, wb) + 2 * 80 > (int)kTmemCols || getenv("ZS_WIN_NO_SEQ")) return 1;
+    p.seq = 1;
+  }
   p.s_col[0] = 0;
-  p.s_col[1] = wa;
-  if (wa + wb <= (int)kTmemCols - 2 * 96) {  // O accumulators 32-column aligned when they fit
+  p.s_col[1] = p.seq ? 0 : wa;
+  const int s_cols = p.seq ? std::max(wa, wb) : wa + wb;
+  if (s_cols <= (int)kTmemCols - 2 * 96) {  // O accumulators 32-column aligned when they fit
     p.o_col[0] = (int)kTmemCols - 2 * 96;
     p.o_col[1] = (int)kTmemCols - 96;
   } else {
@@ -678,6 +708,7 @@ int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, 
     p.o_col[1] = (int)kTmemCols - 80;
   }
   if (p.nrun[1] == 0) p.nt = 1;
+  if (p.nt == 1) p.seq = 0;
   p.nlw = 0;
   for (int X = 0; X < p.nt; ++X)
     for (int w = 0; w < 4; ++w) p.nlw += (X * 128 + w * 32 < S) ? 1 : 0;
