@@ -23,7 +23,12 @@
 //  * Lazy rescaling: O (and its row-sum columns) is rescaled in TMEM, warp-wide, only when a
 //    row max grows by more than ln 256.
 //  * The next item's Bq rows are prefetched from the fp16 table one item ahead and written into
-//    TMEM (tcgen05.st) by the softmax threads once the item's last S' MMA has completed.
+//    TMEM (tcgen05.st) by the softmax threads as soon as the item's last S' MMA has completed,
+//    Q tiles are loaded by their own producer lane (the K / V rings run ahead into the next
+//    item), and the MMA stream runs across items (the next item's first S' before this item's
+//    last PV): at an item boundary only the last PV and the epilogue remain serial.
+//  * Epilogue: the O tile is packed to bf16 in shared memory and leaves through one TMA tensor
+//    store per item (16-byte stores to 128 scattered rows held the softmax warps ~3000 cycles).
 // Roles: warp 0 TMA (lane 0: Q per item + K per chunk, lane 1: V per chunk), warp 1 MMA (whole
 // warp, elected lane), warps 2-3 one-hot key rows per chunk, warps 4-11 softmax.
 #include <cuda_fp16.h>
@@ -43,7 +48,7 @@ constexpr uint32_t kTmemCols = 512;
 constexpr int KST = 3;  // K ring stages
 constexpr int OST = 2;  // one-hot ring stages (generated on chip: no memory latency to hide)
 constexpr int QST = 1;  // Q slots (the next item's Q loads once the last S' of the item completed)
-constexpr int VST = 3;  // V ring stages
+constexpr int VST = 2;  // V ring stages
 constexpr uint32_t TM_S = 0;     // S_w at [w*128, w*128+128)
 constexpr uint32_t TM_O = 256;   // O at [256, 256 + DH), row sums (ones MMA) at [256 + DH, +16)
 constexpr uint32_t TM_BQ = 416;  // Bq: 128 fp16 = 64 columns
@@ -60,7 +65,8 @@ struct Params {
   const int* k_sp;
   float tau;
   __nv_bfloat16* out;
-  int off_q, off_k, off_oh, off_v, off_ml, off_bar, tile, vstage;
+  int off_q, off_k, off_oh, off_v, off_ml, off_ost, off_bar, tile, vstage;
+  int tma_out;  // 1: the O tile leaves through shared memory and one TMA tensor store (no o_rows)
   int trace;
 };
 
@@ -148,6 +154,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     zs_attn_glob_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tq_t,
                         const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tk_t,
                         const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap tv_t,
+                        const __grid_constant__ CUtensorMap to, const __grid_constant__ CUtensorMap to_t,
                         const attng::Params P) {
   using namespace attng;
   using L = Shape<DH>;
@@ -218,18 +225,32 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
     if (warp == 0) {
       // ---------------------------------------------------------- TMA producer
-      if (lane < 2) {
+      if (lane == 2) {
+        // Q tiles on their own lane: the K / V rings run ahead into the next item while the Q slot
+        // waits for this item's last S'; the next item's Q tile is prefetched into L2 meanwhile
+        int k = 0;
+        for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
+          const int i = it % nmb, uh = it / nmb, col = (uh % P.heads) * DH, u = uh / P.heads;
+          const int qs = k % QST;
+          mbar_wait_sleep(&q_empty[qs], ((k / QST) & 1) ^ 1);
+          mbar_expect_tx(&q_full[qs], BQ * DH * 2);
+          uint8_t* q = smem + P.off_q + qs * L::TILE;
+          tma_load_3d(q, &tq, &q_full[qs], col, i * BQ, u);
+          if constexpr (kTail) tma_load_3d(q + L::MAIN, &tq_t, &q_full[qs], col + 64, i * BQ, u);
+          const int it2 = it + gridDim.x;
+          if (it2 < P.items) {
+            const int i2 = it2 % nmb, uh2 = it2 / nmb, col2 = (uh2 % P.heads) * DH, u2 = uh2 / P.heads;
+            asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                             reinterpret_cast<uint64_t>(&tq)), "r"(col2), "r"(i2 * BQ), "r"(u2) : "memory");
+            if constexpr (kTail)
+              asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                               reinterpret_cast<uint64_t>(&tq_t)), "r"(col2 + 64), "r"(i2 * BQ), "r"(u2) : "memory");
+          }
+        }
+      } else if (lane < 2) {
         int k = 0, c = 0;
         for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
           const int i = it % nmb, uh = it / nmb, h = uh % P.heads, u = uh / P.heads, col = h * DH;
-          if (lane == 0) {
-            const int qs = k % QST;
-            mbar_wait_sleep(&q_empty[qs], ((k / QST) & 1) ^ 1);
-            mbar_expect_tx(&q_full[qs], BQ * DH * 2);
-            uint8_t* q = smem + P.off_q + qs * L::TILE;
-            tma_load_3d(q, &tq, &q_full[qs], col, i * BQ, u);
-            if constexpr (kTail) tma_load_3d(q + L::MAIN, &tq_t, &q_full[qs], col + 64, i * BQ, u);
-          }
           const int nc = n_chunks(P, i);
           for (int j = 0; j < nc; ++j, ++c) {
             const int cj = chunk_of(P, i, j);
@@ -266,10 +287,8 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       auto issue_s = [&](int c, int k, int w, bool last) {
         const int ks_ = c % KST, os_ = c % OST, qs = k % QST;
         mbar_wait(&k_full[ks_], (c / KST) & 1);
-        if (lane == 0 && c == first_c + 1) ZG_TR(k, 13);
         if (lane == 0) ZG_T2(k, c - first_c, 4);
         mbar_wait(&oh_full[os_], (c / OST) & 1);
-        if (lane == 0 && c == first_c + 1) ZG_TR(k, 14);
         if (lane == 0) ZG_T2(k, c - first_c, 5);
         tc_fence_after();
         const uint64_t q = dq + qs * TILE16, qt = dqt + qs * TILE16;
@@ -304,31 +323,37 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         umma_commit_elect(o_full);
         umma_commit_elect(&v_empty[vs]);
       };
-      // PV(c-1) is issued right after S'(c): S'(c) goes to the other WG's S buffer, and S'(c)
-      // into S_w always follows PV(c-2) (same WG) in issue order, so P_w is read before it is
-      // overwritten (tcgen05.mma executes in order)
+      // PV(c-1) is issued right after S'(c): S'(c) goes to the other S buffer, and S'(c) into
+      // buffer w always follows PV(c-2) in issue order, so P_w is read before it is overwritten
+      // (tcgen05.mma executes in order).  The stream runs across items: the next item's first
+      // S' is issued before this item's last PV (its Bq is installed as soon as this item's last
+      // S' completed), so the tensor pipe does not drain at item boundaries.
       int npv[2] = {0, 0};
       int pend_c = -1, pend_w = 0, pend_k = 0;
-      bool pend_first = false;
+      bool pend_first = false, pend_last = false;
       auto flush_pv = [&]() {
         mbar_wait(&p_full[pend_w], npv[pend_w] & 1);
         if (pend_first && pend_k > 0) mbar_wait(o_free, (pend_k - 1) & 1);  // previous epilogue read O
         tc_fence_after();
-        if (lane == 0 && pend_c == first_c) ZG_TR(pend_k, 15);
         issue_pv(pend_c, pend_w, pend_first);
         if (lane == 0) ZG_T2(pend_k, pend_c - first_c, 3);
         npv[pend_w]++;
+        if (pend_last) {
+          umma_commit_elect(o_last);  // after the item's last PV: the epilogue's own barrier
+          if (lane == 0) ZG_TR(pend_k, 15);
+        }
+        pend_c = -1;
       };
       int k = 0, c = 0;
       for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
         const int i = it % nmb;
         const int nc = n_chunks(P, i);
-        first_c = c;
         mbar_wait(&q_full[k % QST], (k / QST) & 1);
         mbar_wait(bq_full, k & 1);
         if (lane == 0) ZG_TR(k, 6);
         for (int j = 0; j < nc; ++j, ++c) {
           const int w = c & 1;
+          if (j == 0) first_c = c;
           issue_s(c, k, w, j == nc - 1);
           if (lane == 0 && j < 6) ZG_TR(k, 7 + j);
           if (lane == 0) ZG_T2(k, j, 0);
@@ -337,13 +362,10 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
           pend_w = w;
           pend_k = k;
           pend_first = j == 0;  // first chunk of the item: O starts fresh
+          pend_last = j == nc - 1;
         }
-        // the item's last PV now: its epilogue (and with it the next item's Bq install, which
-        // the next S' waits for) depends on it
-        flush_pv();
-        umma_commit_elect(o_last);  // after the item's last PV: the epilogue's own barrier
-        pend_c = -1;
       }
+      if (pend_c >= 0) flush_pv();
     } else {
       // ---------------------------------------------------------- one-hot key rows (warps 2, 3)
       // chunk c, keys [64*(warp-2), +64): row kr of each SW128 slab = fp16 e_{σk/w} (slab 0) and
@@ -571,6 +593,13 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         const int kvalid = P.S - cj * BQ - 64 * w;  // keys of this half below S
         mbar_wait(&s_full[buf], (c >> 1) & 1);
         tc_fence_after();
+        if (j == nc - 1 && it + G < P.items) {
+          // the item's last S' completed, and with it every read of Bq: install the next item's
+          // rows now, so its first S' does not wait for this chunk's softmax and the epilogue
+          store_bq(bqx, k + 1);
+          load_bq(it + 2 * G, sp_nn, bqx);
+          sp_nn = load_sp(it + 3 * G);
+        }
         if (lane == 0 && wq == 0 && j == 0 && w == 0) ZG_TR(k, 0);
         if (lane == 0 && wq == 0 && w == 0) ZG_T2(k, j, 1);
         const uint32_t s_addr = tmem + TM_S + buf * 128 + lane_off;
@@ -634,7 +663,9 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       // ---- item epilogue: the row sum is O column DH (ones MMA); each half writes its O columns
       // the item's last PV: its own barrier (one completion per item), not an o_full parity,
       // which could already have moved past it by the time this warp waits
+      if (lane == 0 && wq == 0 && w == 0) ZG_TR(k, 13);
       mbar_wait(o_last, k & 1);
+      if (lane == 0 && wq == 0 && w == 0) ZG_TR(k, 14);
       tc_fence_after();
       float inv;
       {
@@ -643,51 +674,60 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         tmem_ld_wait();
         inv = 1.0f / __uint_as_float(l1);
       }
-      bool valid = row < P.S;
-      long long orow_off = (long long)u * P.o_unit_stride + (long long)row * P.ldo;
-      if (valid && P.o_rows) {
-        const int m = P.o_rows[(long long)u * P.S + row];
-        valid = m >= 0;
-        orow_off = (long long)m * P.ldo;
-      }
-      __nv_bfloat16* dst = P.out + orow_off + h * DH + w * OH;
-      {
-        uint32_t a[32];
+      if (P.tma_out) {
+        // O tile -> shared memory (the TMA SW128 / SW32 layout of a [128, 64] + [128, 16] box) ->
+        // one TMA tensor store per item: the stores leave through the async proxy instead of
+        // 16-byte LSU stores to 128 scattered rows, which held this warp for ~3000 cycles
+        constexpr int NQ = OH / 8;  // 16-byte pieces of this half row
+        uint32_t a[32], a8[8];
         tmem_ld32(o_addr + w * OH, a);
-        if constexpr (OH == 40) {
-          uint32_t a8[8];
+        if constexpr (OH == 40)
           asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                        : "=r"(a8[0]), "=r"(a8[1]), "=r"(a8[2]), "=r"(a8[3]), "=r"(a8[4]), "=r"(a8[5]),
                          "=r"(a8[6]), "=r"(a8[7])
                        : "r"(o_addr + w * OH + 32));
-          tmem_ld_wait();
-          if (valid) {
-            uint4* d4 = reinterpret_cast<uint4*>(dst);  // 80-byte aligned row halves: 16-byte stores
+        tmem_ld_wait();
+        uint4 pk[NQ];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) d4[q] = scale_pack8(a + 8 * q, inv);
-            d4[4] = scale_pack8(a8, inv);
-          }
-        } else {
-          tmem_ld_wait();
-          if (valid) {
-            uint4* d4 = reinterpret_cast<uint4*>(dst);
+        for (int q = 0; q < NQ; ++q) pk[q] = scale_pack8(q < 4 ? a + 8 * q : a8, inv);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(o_free);  // O is in registers: the next item's PV may start
+        const bool issuer = warp == 4 && lane == 0;
+        if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
+        named_bar_sync(6, 256);
+        uint8_t* st = smem + P.off_ost;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) d4[q] = scale_pack8(a + 8 * q, inv);
-          }
+        for (int q = 0; q < NQ; ++q) {
+          const int gc = (w * OH) / 8 + q;  // 16-byte chunk of the 2 * DH-byte row
+          const int off = gc < 8 ? r * 128 + ((gc ^ (r & 7)) << 4)
+                                 : L::MAIN + r * 32 + (((gc - 8) ^ ((r >> 2) & 1)) << 4);
+          *reinterpret_cast<uint4*>(st + off) = pk[q];
         }
+        fence_proxy_async_smem();
+        named_bar_sync(6, 256);
+        if (issuer) {
+          asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                           reinterpret_cast<uint64_t>(&to)), "r"(h * DH), "r"(i * BQ), "r"(u), "r"(smem_u32(st))
+                       : "memory");
+          if constexpr (kTail)
+            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                             reinterpret_cast<uint64_t>(&to_t)), "r"(h * DH + 64), "r"(i * BQ), "r"(u),
+                         "r"(smem_u32(st + L::MAIN))
+                         : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (lane == 0 && wq == 0) ZG_TR(k, 4 + w);
+        continue;
       }
-      tc_fence_before();
+      bool valid = row < P.S;
+      long long orow_off = (long long)u * P.o_unit_stride + (long long)row * P.ldo;      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(o_free);
       if (lane == 0 && wq == 0) ZG_TR(k, 4 + w);
-      // next item's bias rows into TMEM once this item's last S' has completed
-      if (it + G < P.items) {
-        store_bq(bqx, k + 1);
-        load_bq(it + 2 * G, sp_nn, bqx);
-        sp_nn = load_sp(it + 3 * G);
-      }
     }
   }
+  if (P.tma_out && warp == 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -740,6 +780,8 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
   p.off_oh = take(OST * OH_BYTES, 1024);
   p.off_v = take(VST * p.vstage, 1024);
   p.off_ml = take(2 * 4 * BQ * 4, 16);
+  p.tma_out = o_rows == nullptr ? 1 : 0;
+  p.off_ost = take(tile, 1024);  // O staging for the TMA store: [128, 64] SW128 + [128, 16] SW32
   p.off_bar = take(512, 8);
   const size_t smem = 1024 + (size_t)off;
   if (smem > 227 * 1024) return 1;
@@ -759,7 +801,7 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
     p.btab = buf;
     p.btab_us = bias_us ? (long long)heads * S * 128 : 0;
   }
-  CUtensorMap m[6];
+  CUtensorMap m[8];
   const uint64_t ncol = (uint64_t)heads * dh;
   int rc = 0;
   rc |= make_tmap_3d_bf16(&m[0], q, ncol, S, units, ldq, qus, 64, BQ, 1, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -774,15 +816,19 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
     m[1] = m[0];
     m[3] = m[2];
   }
+  // output [units, S, heads * dh] (row stride ldo, unit stride ous): the TMA store boxes
+  rc |= make_tmap_3d_bf16(&m[6], out, ncol, S, units, ldo, ous, 64, BQ, 1, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (dh == 80) rc |= make_tmap_3d_bf16(&m[7], out, ncol, S, units, ldo, ous, 16, BQ, 1, CU_TENSOR_MAP_SWIZZLE_32B);
+  else m[7] = m[6];
   if (rc) return ZS_ERR_TMAP;
   int grid = num_sms();
   if (grid > p.items) grid = p.items;
   if (dh == 64) {
     cudaFuncSetAttribute(zs_attn_glob_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    { zs_attn_glob_kernel<64><<<grid, kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p); count_launch(); }
+    { zs_attn_glob_kernel<64><<<grid, kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], p); count_launch(); }
   } else {
     cudaFuncSetAttribute(zs_attn_glob_kernel<80>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    { zs_attn_glob_kernel<80><<<grid, kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p); count_launch(); }
+    { zs_attn_glob_kernel<80><<<grid, kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], p); count_launch(); }
   }
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }

@@ -31,7 +31,7 @@ lib.zs_debug_glob_trace(buf, 64 * 16 + 128)
 a = np.array(buf[:1024], dtype=np.int64).reshape(64, 16)
 t2 = np.array(buf[1024:], dtype=np.int64).reshape(16, 8)
 t0 = a[0, 6]
-names = ["c0_s", "c0_p", "wg0_start", "wg1_start", "wg0_done", "wg1_done", "q+bq", "S0", "S1", "S2", "S3", "S4", "S5", "S1_kful", "S1_ohful", "PV0_go"]
+names = ["c0_s", "c0_p", "wg0_start", "wg1_start", "wg0_done", "wg1_done", "q+bq", "S0", "S1", "S2", "S3", "S4", "S5", "lastP", "epi_go", "PVlast"]
 print("item " + " ".join(f"{n:>9s}" for n in names))
 for k in range(12):
     print(f"{k:4d} " + " ".join(f"{(a[k, c] - t0) if a[k, c] else -1:9d}" for c in range(16)))
