@@ -721,7 +721,39 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         continue;
       }
       bool valid = row < P.S;
-      long long orow_off = (long long)u * P.o_unit_stride + (long long)row * P.ldo;      tc_fence_before();
+      long long orow_off = (long long)u * P.o_unit_stride + (long long)row * P.ldo;
+      if (valid && P.o_rows) {
+        const int m = P.o_rows[(long long)u * P.S + row];
+        valid = m >= 0;
+        orow_off = (long long)m * P.ldo;
+      }
+      __nv_bfloat16* dst = P.out + orow_off + h * DH + w * OH;
+      {
+        uint32_t a[32];
+        tmem_ld32(o_addr + w * OH, a);
+        if constexpr (OH == 40) {
+          uint32_t a8[8];
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(a8[0]), "=r"(a8[1]), "=r"(a8[2]), "=r"(a8[3]), "=r"(a8[4]), "=r"(a8[5]),
+                         "=r"(a8[6]), "=r"(a8[7])
+                       : "r"(o_addr + w * OH + 32));
+          tmem_ld_wait();
+          if (valid) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst);  // 80-byte aligned row halves: 16-byte stores
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d4[q] = scale_pack8(a + 8 * q, inv);
+            d4[4] = scale_pack8(a8, inv);
+          }
+        } else {
+          tmem_ld_wait();
+          if (valid) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d4[q] = scale_pack8(a + 8 * q, inv);
+          }
+        }
+      }
+      tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(o_free);
       if (lane == 0 && wq == 0) ZG_TR(k, 4 + w);

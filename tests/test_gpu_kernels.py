@@ -354,17 +354,19 @@ def test_im2col3x3_tap_major():
     assert torch.equal(out.float(), ref)
 
 
-def test_attention_output_row_map_and_pad_helpers():
+@pytest.mark.parametrize("S,w,tile", [(196, 14, 32), (1024, 32, 128)])
+def test_attention_output_row_map_and_pad_helpers(S, w, tile):
     """zs_stripe_attn_fwd_rows writes row r of unit u to out[o_rows[u*S+r]] (skips -1) and equals the
-    plain layout otherwise; invert_rows / fill_flagged_rows (window pad-token skipping)."""
+    plain layout otherwise (window kernel, and the global kernel whose plain layout leaves through a
+    TMA tensor store); invert_rows / fill_flagged_rows (window pad-token skipping)."""
     g = torch.Generator().manual_seed(21)
-    units, heads, S, dh, w = 6, 2, 196, 80, 14
+    units, heads, dh = 6, 2, 80
     C = heads * dh
     qkv = torch.randn(units * S, 3 * C, generator=g).bfloat16().to(DEV)
     bh = (0.5 * torch.randn(heads, S, w, generator=g)).to(DEV)
     bw = (0.5 * torch.randn(heads, S, w, generator=g)).to(DEV)
     sp = torch.stack([torch.randperm(S, generator=g) for _ in range(units)]).int().to(DEV)
-    kw = dict(units=units, heads=heads, sq=S, sk=S, dh=dh, bh=bh, bw=bw, q_sp=sp, k_sp=sp, b_row=32, b_col=32,
+    kw = dict(units=units, heads=heads, sq=S, sk=S, dh=dh, bh=bh, bw=bw, q_sp=sp, k_sp=sp, b_row=tile, b_col=tile,
               prefix=2, tau=dh ** -0.5)
     full = K.stripe_attn(qkv[:, :C], qkv[:, C:2 * C], qkv[:, 2 * C:], **kw)
     keep = (torch.rand(units * S, generator=g) < 0.8).to(DEV)
