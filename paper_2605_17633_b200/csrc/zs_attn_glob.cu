@@ -29,6 +29,8 @@
 //    last PV): at an item boundary only the last PV and the epilogue remain serial.
 //  * Epilogue: the O tile is packed to bf16 in shared memory and leaves through one TMA tensor
 //    store per item (16-byte stores to 128 scattered rows held the softmax warps ~3000 cycles).
+//    O is double-buffered in TMEM (S 256 + 2 x O 96 + Bq 64 = 512 columns), so an item's epilogue
+//    runs after the next item's first chunk, when its last PV has long completed.
 // Roles: warp 0 TMA (lane 0: Q per item + K per chunk, lane 1: V per chunk), warp 1 MMA (whole
 // warp, elected lane), warps 2-3 one-hot key rows per chunk, warps 4-11 softmax.
 #include <cuda_fp16.h>
@@ -50,8 +52,9 @@ constexpr int OST = 2;  // one-hot ring stages (generated on chip: no memory lat
 constexpr int QST = 1;  // Q slots (the next item's Q loads once the last S' of the item completed)
 constexpr int VST = 2;  // V ring stages
 constexpr uint32_t TM_S = 0;     // S_w at [w*128, w*128+128)
-constexpr uint32_t TM_O = 256;   // O at [256, 256 + DH), row sums (ones MMA) at [256 + DH, +16)
-constexpr uint32_t TM_BQ = 416;  // Bq: 128 fp16 = 64 columns
+constexpr uint32_t TM_O = 256;   // O_b at [256 + 96b, + DH), row sums (ones atom) at [+DH, +DH+16); b = item & 1
+constexpr uint32_t TM_OS = 96;   // columns per O buffer
+constexpr uint32_t TM_BQ = 448;  // Bq: 128 fp16 = 64 columns
 constexpr int OH_BYTES = 2 * BQ * 128;  // two 64-column SW128 slabs (e_ky | e_kx)
 constexpr int VATOM = BQ * 32;          // V: MN-major SW32 atoms of 16 columns x 128 keys
 
@@ -172,8 +175,8 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
   uint64_t* s_full = bar + 24;   // [wg]
   uint64_t* p_full = bar + 26;   // [S buffer]  8 softmax warps: P of the chunk in TMEM
   uint64_t* o_full = bar + 28;   // PV of a chunk completed (one completion per chunk)
-  uint64_t* o_last = bar + 29;   // the item's last PV completed (one completion per item)
-  uint64_t* o_free = bar + 30;   // 8 warps: O_0 / O_1 read by the item's epilogue
+  uint64_t* o_last = bar + 42;   // [O buffer] the item's last PV completed (one completion per item)
+  uint64_t* o_free = bar + 40;   // [O buffer] 8 warps: O_b read by the epilogue of its item
   uint64_t* bq_full = bar + 31;  // 8 warps: the item's Bq rows are in TMEM
   uint64_t* bq_free = bar + 32;  // the item's last S' completed (Bq may be replaced)
   uint64_t* oh_empty = bar + 36; // [OST] S' of the chunk done: one-hot stage free
@@ -196,7 +199,8 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       mbar_init(&p_full[s], 8);
     }
     mbar_init(o_full, 1);
-    mbar_init(o_last, 1);
+    mbar_init(&o_last[0], 1);
+    mbar_init(&o_last[1], 1);
     for (int s = 0; s < KST; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -209,7 +213,8 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
-    mbar_init(o_free, 8);
+    mbar_init(&o_free[0], 8);
+    mbar_init(&o_free[1], 8);
     mbar_init(bq_full, 8);
     mbar_init(bq_free, 1);
     fence_mbar_init();
@@ -309,13 +314,13 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
           umma_commit_elect(bq_free);
         }
       };
-      auto issue_pv = [&](int c, int w, bool first) {
+      auto issue_pv = [&](int c, int w, bool first, int ob) {
         const int vs = c % VST;
         mbar_wait(&v_full[vs], (c / VST) & 1);
         tc_fence_after();
         const uint64_t v = dv + vs * (L::VSTAGE >> 4);
         const uint32_t a0 = tmem + TM_S + w * 128;
-        const uint32_t d = tmem + TM_O;
+        const uint32_t d = tmem + TM_O + ob * TM_OS;
         // [O | row sums] (+)= P . [V | 1]: one N = DH + 16 MMA per 16 keys
 #pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks)
@@ -333,13 +338,14 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       bool pend_first = false, pend_last = false;
       auto flush_pv = [&]() {
         mbar_wait(&p_full[pend_w], npv[pend_w] & 1);
-        if (pend_first && pend_k > 0) mbar_wait(o_free, (pend_k - 1) & 1);  // previous epilogue read O
+        // O_b is reused every second item: the epilogue of item k - 2 must have read it
+        if (pend_first && pend_k > 1) mbar_wait(&o_free[pend_k & 1], ((pend_k >> 1) - 1) & 1);
         tc_fence_after();
-        issue_pv(pend_c, pend_w, pend_first);
+        issue_pv(pend_c, pend_w, pend_first, pend_k & 1);
         if (lane == 0) ZG_T2(pend_k, pend_c - first_c, 3);
         npv[pend_w]++;
         if (pend_last) {
-          umma_commit_elect(o_last);  // after the item's last PV: the epilogue's own barrier
+          umma_commit_elect(&o_last[pend_k & 1]);  // after the item's last PV: the epilogue's own barrier
           if (lane == 0) ZG_TR(pend_k, 15);
         }
         pend_c = -1;
@@ -473,7 +479,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     const int wq = warp & 3;
     const int r = wq * 32 + lane;  // row within the tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    const uint32_t o_addr = tmem + TM_O + lane_off;
+    uint32_t o_addr = tmem + TM_O + lane_off;  // O buffer of the current item (item & 1)
     const uint32_t bq_addr = tmem + TM_BQ + w * 32 + lane_off;  // this half's 64 fp16 bias columns
     float* xch = reinterpret_cast<float*>(smem + P.off_ml);     // [chunk parity][half][BQ] partial max
     const uint32_t pair_bar = 1 + wq;
@@ -574,6 +580,109 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       }
     };
 
+    // ---- item epilogue (item k, O buffer k & 1): run after the NEXT item's first chunk, so the
+    // item's last PV completes under that chunk's softmax; the row sum is O column DH (ones atom)
+    auto epilogue = [&](const int k, const int i, const int h, const int u) {
+      const int row = i * BQ + r;
+      const uint32_t o_addr = tmem + TM_O + (k & 1) * TM_OS + lane_off;
+      uint64_t* const o_free_k = &o_free[k & 1];
+      // the item's last PV: its own barrier (one completion per item), not an o_full parity,
+      // which could already have moved past it by the time this warp waits
+      if (lane == 0 && wq == 0 && w == 0) ZG_TR(k, 13);
+      mbar_wait(&o_last[k & 1], (k >> 1) & 1);  // per buffer: a one-chunk next item cannot overtake it
+      if (lane == 0 && wq == 0 && w == 0) ZG_TR(k, 14);
+      tc_fence_after();
+      float inv;
+      {
+        uint32_t l1;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(l1) : "r"(o_addr + DH));
+        tmem_ld_wait();
+        inv = 1.0f / __uint_as_float(l1);
+      }
+      if (P.tma_out) {
+        // O tile -> shared memory (the TMA SW128 / SW32 layout of a [128, 64] + [128, 16] box) ->
+        // one TMA tensor store per item: the stores leave through the async proxy instead of
+        // 16-byte LSU stores to 128 scattered rows, which held this warp for ~3000 cycles
+        constexpr int NQ = OH / 8;  // 16-byte pieces of this half row
+        uint32_t a[32], a8[8];
+        tmem_ld32(o_addr + w * OH, a);
+        if constexpr (OH == 40)
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(a8[0]), "=r"(a8[1]), "=r"(a8[2]), "=r"(a8[3]), "=r"(a8[4]), "=r"(a8[5]),
+                         "=r"(a8[6]), "=r"(a8[7])
+                       : "r"(o_addr + w * OH + 32));
+        tmem_ld_wait();
+        uint4 pk[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) pk[q] = scale_pack8(q < 4 ? a + 8 * q : a8, inv);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(o_free_k);  // O is in registers: the next item's PV may start
+        const bool issuer = warp == 4 && lane == 0;
+        if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
+        named_bar_sync(6, 256);
+        uint8_t* st = smem + P.off_ost;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int gc = (w * OH) / 8 + q;  // 16-byte chunk of the 2 * DH-byte row
+          const int off = gc < 8 ? r * 128 + ((gc ^ (r & 7)) << 4)
+                                 : L::MAIN + r * 32 + (((gc - 8) ^ ((r >> 2) & 1)) << 4);
+          *reinterpret_cast<uint4*>(st + off) = pk[q];
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(6, 256);
+        if (issuer) {
+          asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                           reinterpret_cast<uint64_t>(&to)), "r"(h * DH), "r"(i * BQ), "r"(u), "r"(smem_u32(st))
+                       : "memory");
+          if constexpr (kTail)
+            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                             reinterpret_cast<uint64_t>(&to_t)), "r"(h * DH + 64), "r"(i * BQ), "r"(u),
+                         "r"(smem_u32(st + L::MAIN))
+                         : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        if (lane == 0 && wq == 0) ZG_TR(k, 4 + w);
+        return;
+      }
+      bool valid = row < P.S;
+      long long orow_off = (long long)u * P.o_unit_stride + (long long)row * P.ldo;
+      if (valid && P.o_rows) {
+        const int m = P.o_rows[(long long)u * P.S + row];
+        valid = m >= 0;
+        orow_off = (long long)m * P.ldo;
+      }
+      __nv_bfloat16* dst = P.out + orow_off + h * DH + w * OH;
+      {
+        uint32_t a[32];
+        tmem_ld32(o_addr + w * OH, a);
+        if constexpr (OH == 40) {
+          uint32_t a8[8];
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(a8[0]), "=r"(a8[1]), "=r"(a8[2]), "=r"(a8[3]), "=r"(a8[4]), "=r"(a8[5]),
+                         "=r"(a8[6]), "=r"(a8[7])
+                       : "r"(o_addr + w * OH + 32));
+          tmem_ld_wait();
+          if (valid) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst);  // 80-byte aligned row halves: 16-byte stores
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d4[q] = scale_pack8(a + 8 * q, inv);
+            d4[4] = scale_pack8(a8, inv);
+          }
+        } else {
+          tmem_ld_wait();
+          if (valid) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d4[q] = scale_pack8(a + 8 * q, inv);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(o_free_k);
+      if (lane == 0 && wq == 0) ZG_TR(k, 4 + w);
+    };
     const int G = gridDim.x;
     uint4 bqx[8];
     load_bq(blockIdx.x, load_sp(blockIdx.x), bqx);
@@ -581,10 +690,11 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     load_bq(blockIdx.x + G, load_sp(blockIdx.x + G), bqx);  // next item's rows, in flight during this item
     int sp_nn = load_sp(blockIdx.x + 2 * G);                  // and the row index of the one after
     int k = 0, c = 0;
+    int kp = -1, ip = 0, hp = 0, up = 0;  // the previous item, whose epilogue is pending
     for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
       const int i = it % nmb, uh = it / nmb, h = uh % P.heads, u = uh / P.heads;
       const int nc = n_chunks(P, i);
-      const int row = i * BQ + r;
+      o_addr = tmem + TM_O + (k & 1) * TM_OS + lane_off;
       if (lane == 0 && wq == 0) ZG_TR(k, 2 + w);
       float m_ref = -INFINITY;
       for (int j = 0; j < nc; ++j, ++c) {
@@ -659,105 +769,14 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         if (lane == 0) mbar_arrive(&p_full[buf]);
         if (lane == 0 && wq == 0 && j == 0 && w == 0) ZG_TR(k, 1);
         if (lane == 0 && wq == 0 && w == 0) ZG_T2(k, j, 2);
-      }
-      // ---- item epilogue: the row sum is O column DH (ones MMA); each half writes its O columns
-      // the item's last PV: its own barrier (one completion per item), not an o_full parity,
-      // which could already have moved past it by the time this warp waits
-      if (lane == 0 && wq == 0 && w == 0) ZG_TR(k, 13);
-      mbar_wait(o_last, k & 1);
-      if (lane == 0 && wq == 0 && w == 0) ZG_TR(k, 14);
-      tc_fence_after();
-      float inv;
-      {
-        uint32_t l1;
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(l1) : "r"(o_addr + DH));
-        tmem_ld_wait();
-        inv = 1.0f / __uint_as_float(l1);
-      }
-      if (P.tma_out) {
-        // O tile -> shared memory (the TMA SW128 / SW32 layout of a [128, 64] + [128, 16] box) ->
-        // one TMA tensor store per item: the stores leave through the async proxy instead of
-        // 16-byte LSU stores to 128 scattered rows, which held this warp for ~3000 cycles
-        constexpr int NQ = OH / 8;  // 16-byte pieces of this half row
-        uint32_t a[32], a8[8];
-        tmem_ld32(o_addr + w * OH, a);
-        if constexpr (OH == 40)
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                       : "=r"(a8[0]), "=r"(a8[1]), "=r"(a8[2]), "=r"(a8[3]), "=r"(a8[4]), "=r"(a8[5]),
-                         "=r"(a8[6]), "=r"(a8[7])
-                       : "r"(o_addr + w * OH + 32));
-        tmem_ld_wait();
-        uint4 pk[NQ];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) pk[q] = scale_pack8(q < 4 ? a + 8 * q : a8, inv);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(o_free);  // O is in registers: the next item's PV may start
-        const bool issuer = warp == 4 && lane == 0;
-        if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
-        named_bar_sync(6, 256);
-        uint8_t* st = smem + P.off_ost;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          const int gc = (w * OH) / 8 + q;  // 16-byte chunk of the 2 * DH-byte row
-          const int off = gc < 8 ? r * 128 + ((gc ^ (r & 7)) << 4)
-                                 : L::MAIN + r * 32 + (((gc - 8) ^ ((r >> 2) & 1)) << 4);
-          *reinterpret_cast<uint4*>(st + off) = pk[q];
-        }
-        fence_proxy_async_smem();
-        named_bar_sync(6, 256);
-        if (issuer) {
-          asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
-                           reinterpret_cast<uint64_t>(&to)), "r"(h * DH), "r"(i * BQ), "r"(u), "r"(smem_u32(st))
-                       : "memory");
-          if constexpr (kTail)
-            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
-                             reinterpret_cast<uint64_t>(&to_t)), "r"(h * DH + 64), "r"(i * BQ), "r"(u),
-                         "r"(smem_u32(st + L::MAIN))
-                         : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-        if (lane == 0 && wq == 0) ZG_TR(k, 4 + w);
-        continue;
-      }
-      bool valid = row < P.S;
-      long long orow_off = (long long)u * P.o_unit_stride + (long long)row * P.ldo;
-      if (valid && P.o_rows) {
-        const int m = P.o_rows[(long long)u * P.S + row];
-        valid = m >= 0;
-        orow_off = (long long)m * P.ldo;
-      }
-      __nv_bfloat16* dst = P.out + orow_off + h * DH + w * OH;
-      {
-        uint32_t a[32];
-        tmem_ld32(o_addr + w * OH, a);
-        if constexpr (OH == 40) {
-          uint32_t a8[8];
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                       : "=r"(a8[0]), "=r"(a8[1]), "=r"(a8[2]), "=r"(a8[3]), "=r"(a8[4]), "=r"(a8[5]),
-                         "=r"(a8[6]), "=r"(a8[7])
-                       : "r"(o_addr + w * OH + 32));
-          tmem_ld_wait();
-          if (valid) {
-            uint4* d4 = reinterpret_cast<uint4*>(dst);  // 80-byte aligned row halves: 16-byte stores
-#pragma unroll
-            for (int q = 0; q < 4; ++q) d4[q] = scale_pack8(a + 8 * q, inv);
-            d4[4] = scale_pack8(a8, inv);
-          }
-        } else {
-          tmem_ld_wait();
-          if (valid) {
-            uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) d4[q] = scale_pack8(a + 8 * q, inv);
-          }
+        if (j == 0 && kp >= 0) {
+          epilogue(kp, ip, hp, up);
+          kp = -1;
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(o_free);
-      if (lane == 0 && wq == 0) ZG_TR(k, 4 + w);
+      kp = k, ip = i, hp = h, up = u;
     }
+    if (kp >= 0) epilogue(kp, ip, hp, up);
   }
   if (P.tma_out && warp == 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();

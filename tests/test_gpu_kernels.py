@@ -289,7 +289,7 @@ def test_attention_window_kernels_agree(r, monkeypatch):
 
 
 @pytest.mark.parametrize("dh", [64, 80])
-@pytest.mark.parametrize("r", [0.2, 0.4, 1.0])
+@pytest.mark.parametrize("r", [0.0, 0.2, 0.4, 1.0])
 def test_attention_global(dh, r):
     assert _attn_case(2, 2, 4096, dh, 64, 128, r) < 1e-2
 
