@@ -132,3 +132,21 @@ def test_module_api_mirrors_sam_parameter_tree():
     assert sd["neck.3.bias"].shape == (256,)
     assert [b.kind for b in enc.blocks].count("global") == 4
     assert len(sd) == 3 + 12 * 14 + 6  # SAM vit_b image encoder: 177 entries
+
+
+def test_from_sam_image_encoder_copies_config_and_weights():
+    """modules.from_sam_image_encoder reads a SAM ImageEncoderViT's configuration from its attributes
+    (duck-typed; here a module with SAM's tree) and loads its state_dict."""
+    import torch
+
+    from paper_2605_17633_b200 import modules as M
+
+    torch.manual_seed(0)
+    src = M.SparseSAMImageEncoderViT(img_size=320, embed_dim=128, depth=3, num_heads=2, window_size=6,
+                                     global_attn_indexes=(1,), use_rel_pos=True, rel_pos_zero_init=False)
+    dst = M.from_sam_image_encoder(src, density=0.3, keep_fraction=0.5)
+    assert [b.kind for b in dst.blocks] == ["local", "global", "local"]
+    assert dst.blocks[0].window_size == 6 and dst.blocks[0].attn.density == 0.3
+    assert dst.blocks[2].mlp.keep_fraction == 0.5
+    for k, v in src.state_dict().items():
+        assert torch.equal(dst.state_dict()[k], v), k
