@@ -13,15 +13,17 @@
 //    keys, generated in shared memory).  logit = tau * S', so the softmax does no gathers.
 //  * Chunk c's S' goes to TMEM S buffer c % 2, so S'(c + 1) is computed while chunk c is in
 //    the softmax.  All 8 softmax warps work on every chunk: the two warps of a TMEM lane
-//    quarter (warps 4 + q and 8 + q) split its 128 keys (64 each) and exchange partial row
-//    maxima through shared memory (one 64-thread named barrier per chunk).
+//    quarter (warps 4 + q and 8 + q) split its 128 keys (64 each), and each key half runs its
+//    own online softmax (reference max, O accumulator O_half with row sums, P -> its own PV
+//    MMAs), with no per-chunk exchange: the two warps of an SMSP drift out of phase, so one's
+//    row max overlaps the other's exponentials.  The halves merge once per item in the epilogue.
 //  * P (bf16) overwrites the chunk's S columns in TMEM (half w's 64 keys at columns [64w, 64w+32),
-//    inside its own S columns) and is the A operand of the PV MMA.  One O accumulator per CTA;
+//    inside its own S columns) and is the A operand of that half's PV MMAs into O_half;
 //    the PV is ONE N = DH + 16 MMA per 16 keys: V is staged as MN-major SW32 atoms of 16 columns
 //    followed by an atom of bf16 ones, so the 16 extra O columns hold the row sums (of the bf16 P
 //    exactly as applied to V).  (N = 16 MMAs cost ~26 cycles each, as much as N = 64.)
-//  * Lazy rescaling: O (and its row-sum columns) is rescaled in TMEM, warp-wide, only when a
-//    row max grows by more than ln 256.
+//  * Lazy rescaling: O_half (and its row-sum columns) is rescaled in TMEM, warp-wide, only when
+//    the half's row max grows by more than ln 256.
 //  * The next item's Bq rows are prefetched from the fp16 table one item ahead and written into
 //    TMEM (tcgen05.st) by the softmax threads as soon as the item's last S' MMA has completed,
 //    Q tiles are loaded by their own producer lane (the K / V rings run ahead into the next
@@ -29,8 +31,8 @@
 //    last PV): at an item boundary only the last PV and the epilogue remain serial.
 //  * Epilogue: the O tile is packed to bf16 in shared memory and leaves through one TMA tensor
 //    store per item (16-byte stores to 128 scattered rows held the softmax warps ~3000 cycles).
-//    O is double-buffered in TMEM (S 256 + 2 x O 96 + Bq 64 = 512 columns), so an item's epilogue
-//    runs after the next item's first chunk, when its last PV has long completed.
+//    TMEM: S 256 + O_0 96 + O_1 96 + Bq 64 = 512 columns.  An item's epilogue runs after the
+//    next item's first chunk, when its last PVs have long completed.
 // Roles: warp 0 TMA (lane 0: Q per item + K per chunk, lane 1: V per chunk), warp 1 MMA (whole
 // warp, elected lane), warps 2-3 one-hot key rows per chunk, warps 4-11 softmax.
 #include <cuda_fp16.h>
@@ -173,10 +175,10 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
   uint64_t* v_full = bar + 16;   // [VST]
   uint64_t* v_empty = bar + 20;  // [VST]
   uint64_t* s_full = bar + 24;   // [wg]
-  uint64_t* p_full = bar + 26;   // [S buffer]  8 softmax warps: P of the chunk in TMEM
-  uint64_t* o_full = bar + 28;   // PV of a chunk completed (one completion per chunk)
-  uint64_t* o_last = bar + 42;   // [O buffer] the item's last PV completed (one completion per item)
-  uint64_t* o_free = bar + 40;   // [O buffer] 8 warps: O_b read by the epilogue of its item
+  uint64_t* p_full = bar + 44;   // [S buffer][half] 4 softmax warps: this half's P of the chunk in TMEM
+  uint64_t* o_full = bar + 48;   // [half] PV_half of a chunk completed (one completion per chunk)
+  uint64_t* o_last = bar + 29;   // the item's last PVs completed (one completion per item)
+  uint64_t* o_free = bar + 30;   // 8 warps: O_0 / O_1 read by the item's epilogue
   uint64_t* bq_full = bar + 31;  // 8 warps: the item's Bq rows are in TMEM
   uint64_t* bq_free = bar + 32;  // the item's last S' completed (Bq may be replaced)
   uint64_t* oh_empty = bar + 36; // [OST] S' of the chunk done: one-hot stage free
@@ -196,11 +198,11 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 8);
+      mbar_init(&p_full[2 * s], 4);
+      mbar_init(&p_full[2 * s + 1], 4);
+      mbar_init(&o_full[s], 1);
     }
-    mbar_init(o_full, 1);
-    mbar_init(&o_last[0], 1);
-    mbar_init(&o_last[1], 1);
+    mbar_init(o_last, 1);
     for (int s = 0; s < KST; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -213,8 +215,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
-    mbar_init(&o_free[0], 8);
-    mbar_init(&o_free[1], 8);
+    mbar_init(o_free, 8);
     mbar_init(bq_full, 8);
     mbar_init(bq_free, 1);
     fence_mbar_init();
@@ -314,19 +315,17 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
           umma_commit_elect(bq_free);
         }
       };
-      auto issue_pv = [&](int c, int w, bool first, int ob) {
+      // PV of one key half (keys [64x, 64x + 64) of chunk c) into that half's accumulator O_x:
+      // [O_x | row sums] (+)= P_x . [V | 1], one N = DH + 16 MMA per 16 keys
+      auto issue_pv_half = [&](int c, int w, bool first, int x) {
         const int vs = c % VST;
-        mbar_wait(&v_full[vs], (c / VST) & 1);
-        tc_fence_after();
         const uint64_t v = dv + vs * (L::VSTAGE >> 4);
-        const uint32_t a0 = tmem + TM_S + w * 128;
-        const uint32_t d = tmem + TM_O + ob * TM_OS;
-        // [O | row sums] (+)= P . [V | 1]: one N = DH + 16 MMA per 16 keys
+        const uint32_t a0 = tmem + TM_S + w * 128 + 64 * x;  // half x's P: its own S columns
+        const uint32_t d = tmem + TM_O + x * TM_OS;
 #pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks)
-          umma_ts(d, a0 + 8 * ks + (ks >= 4 ? 32 : 0), v + ks * (16 * 32 / 16), id_pv, (!first || ks > 0) ? 1u : 0u);
-        umma_commit_elect(o_full);
-        umma_commit_elect(&v_empty[vs]);
+        for (int ks = 0; ks < 4; ++ks)
+          umma_ts(d, a0 + 8 * ks, v + (4 * x + ks) * (16 * 32 / 16), id_pv, (!first || ks > 0) ? 1u : 0u);
+        umma_commit_elect(&o_full[x]);
       };
       // PV(c-1) is issued right after S'(c): S'(c) goes to the other S buffer, and S'(c) into
       // buffer w always follows PV(c-2) in issue order, so P_w is read before it is overwritten
@@ -337,15 +336,21 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       int pend_c = -1, pend_w = 0, pend_k = 0;
       bool pend_first = false, pend_last = false;
       auto flush_pv = [&]() {
-        mbar_wait(&p_full[pend_w], npv[pend_w] & 1);
-        // O_b is reused every second item: the epilogue of item k - 2 must have read it
-        if (pend_first && pend_k > 1) mbar_wait(&o_free[pend_k & 1], ((pend_k >> 1) - 1) & 1);
-        tc_fence_after();
-        issue_pv(pend_c, pend_w, pend_first, pend_k & 1);
+        const int vs = pend_c % VST;
+        mbar_wait(&v_full[vs], (pend_c / VST) & 1);
+        if (pend_first && pend_k > 0) mbar_wait(o_free, (pend_k - 1) & 1);  // previous epilogue read O_0 / O_1
+        // each half's PV as soon as that half's P is in TMEM (the halves run their softmax independently)
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+          mbar_wait(&p_full[2 * pend_w + x], npv[pend_w] & 1);
+          tc_fence_after();
+          issue_pv_half(pend_c, pend_w, pend_first, x);
+        }
+        umma_commit_elect(&v_empty[vs]);
         if (lane == 0) ZG_T2(pend_k, pend_c - first_c, 3);
         npv[pend_w]++;
         if (pend_last) {
-          umma_commit_elect(&o_last[pend_k & 1]);  // after the item's last PV: the epilogue's own barrier
+          umma_commit_elect(o_last);  // after the item's last PVs: the epilogue's own barrier
           if (lane == 0) ZG_TR(pend_k, 15);
         }
         pend_c = -1;
@@ -470,18 +475,19 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
     // ------------------------------------------------------------ softmax warpgroups
-    // every chunk is processed by all 8 softmax warps: warp (half w, quarter wq) owns rows
-    // wq*32 + lane (TMEM lane quarter) and key columns [64w, 64w + 64) of the chunk; the two
-    // halves of a row exchange their partial max through shared memory (pair barrier 1 + wq)
-    // and keep partial row sums, merged once per item.  One O accumulator: half w rescales /
-    // reads O columns [40w, 40w + 40).
+    // Half w (warps 4 + 4w .. 7 + 4w) owns key columns [64w, 64w + 64) of every chunk with its own
+    // online softmax: reference max m_w, accumulator O_w (+ row sums), P_w -> p_full[buf][w].  The
+    // halves never synchronise per chunk (no partial-max exchange), so the two warps of an SMSP
+    // drift out of phase and one's row max overlaps the other's exponentials; they merge once per
+    // item: out = (a_0 O_0 + a_1 O_1) / (a_0 l_0 + a_1 l_1), a_w = 2^((m_w - max(m_0, m_1)) log2 e).
+    // Thread = row wq*32 + lane (TMEM lane quarter of the warp).
     const int w = (warp - 4) >> 2;
     const int wq = warp & 3;
     const int r = wq * 32 + lane;  // row within the tile == TMEM lane
     const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    uint32_t o_addr = tmem + TM_O + lane_off;  // O buffer of the current item (item & 1)
-    const uint32_t bq_addr = tmem + TM_BQ + w * 32 + lane_off;  // this half's 64 fp16 bias columns
-    float* xch = reinterpret_cast<float*>(smem + P.off_ml);     // [chunk parity][half][BQ] partial max
+    const uint32_t o_mine = tmem + TM_O + w * TM_OS + lane_off;  // O_w
+    const uint32_t bq_addr = tmem + TM_BQ + w * 32 + lane_off;    // this half's 64 fp16 bias columns
+    float* xch = reinterpret_cast<float*>(smem + P.off_ml);       // [item parity][half][BQ] reference max
     const uint32_t pair_bar = 1 + wq;
     constexpr float L2E = 1.4426950408889634f;
     constexpr float kThr = 5.545177444479562f;  // ln 256
@@ -532,92 +538,76 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(bq_full);
     };
-    // O columns this half rescales: half 0 [0, OH), half 1 [OH, DH + 16) incl. the row-sum columns
-    // [DH, DH + 16) of the ones MMA; OH = DH / 2 (40 or 32)
-    constexpr int OH = DH / 2;
-    auto ld_x8 = [&](uint32_t a, uint32_t (&r)[8]) {
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                   : "r"(a));
-    };
-    auto st_x8 = [&](uint32_t a, const uint32_t (&r)[8]) {
-      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(a), "r"(r[0]),
-                   "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-                   : "memory");
-    };
-    auto scale32 = [&](uint32_t a, float alpha) {
-      uint32_t pr[32];
-      tmem_ld32(a, pr);
-      tmem_ld_wait();
-#pragma unroll
-      for (int q = 0; q < 32; ++q) pr[q] = __float_as_uint(__uint_as_float(pr[q]) * alpha);
-      tmem_st32(a, pr);
-    };
-    auto scale16 = [&](uint32_t a, float alpha) {
-      uint32_t pr[16];
-      tmem_ld16(a, pr);
-      tmem_ld_wait();
-#pragma unroll
-      for (int q = 0; q < 16; ++q) pr[q] = __float_as_uint(__uint_as_float(pr[q]) * alpha);
-      tmem_st16(a, pr);
-    };
-    auto scale8 = [&](uint32_t a, float alpha) {
-      uint32_t pr[8];
-      ld_x8(a, pr);
-      tmem_ld_wait();
-#pragma unroll
-      for (int q = 0; q < 8; ++q) pr[q] = __float_as_uint(__uint_as_float(pr[q]) * alpha);
-      st_x8(a, pr);
-    };
+    // O_w (DH + 16 columns incl. the row sums) *= alpha, 8 columns at a time (S values are live)
     auto o_scale = [&](float alpha) {
-      if (w == 0) {
-        scale32(o_addr, alpha);
-        if constexpr (OH == 40) scale8(o_addr + 32, alpha);
-      } else {
-        scale32(o_addr + OH, alpha);
-        scale16(o_addr + OH + 32, alpha);
-        if constexpr (OH == 40) scale8(o_addr + OH + 48, alpha);
+#pragma unroll
+      for (int c0 = 0; c0 < DH + 16; c0 += 8) {
+        uint32_t pr[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(pr[0]), "=r"(pr[1]), "=r"(pr[2]), "=r"(pr[3]), "=r"(pr[4]), "=r"(pr[5]), "=r"(pr[6]),
+                       "=r"(pr[7])
+                     : "r"(o_mine + c0));
+        tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) pr[q] = __float_as_uint(__uint_as_float(pr[q]) * alpha);
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(o_mine + c0),
+                     "r"(pr[0]), "r"(pr[1]), "r"(pr[2]), "r"(pr[3]), "r"(pr[4]), "r"(pr[5]), "r"(pr[6]), "r"(pr[7])
+                     : "memory");
       }
     };
+    // output columns [w*OH, w*OH + OH) of this row; OH = DH / 2 (40 or 32)
+    constexpr int OH = DH / 2;
+    constexpr int NQ = OH / 8;  // 16-byte pieces of this half row
+    auto ld_cols = [&](uint32_t a, uint32_t (&v)[OH]) {
+      tmem_ld32(a, *reinterpret_cast<uint32_t(*)[32]>(v));
+      if constexpr (OH == 40)
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]),
+                       "=r"(v[39])
+                     : "r"(a + 32));
+    };
 
-    // ---- item epilogue (item k, O buffer k & 1): run after the NEXT item's first chunk, so the
-    // item's last PV completes under that chunk's softmax; the row sum is O column DH (ones atom)
-    auto epilogue = [&](const int k, const int i, const int h, const int u) {
+    // ---- item epilogue: merge the halves, normalise, store this half's output columns
+    auto epilogue = [&](const int k, const int i, const int h, const int u, const float mref) {
       const int row = i * BQ + r;
-      const uint32_t o_addr = tmem + TM_O + (k & 1) * TM_OS + lane_off;
-      uint64_t* const o_free_k = &o_free[k & 1];
-      // the item's last PV: its own barrier (one completion per item), not an o_full parity,
-      // which could already have moved past it by the time this warp waits
+      float* xk = xch + (k & 1) * 2 * BQ;
+      xk[w * BQ + r] = mref;
+      named_bar_sync(pair_bar, 64);
+      const float mo = xk[(w ^ 1) * BQ + r];
+      const float m = fmaxf(mref, mo);
+      const float a_me = (mref == -INFINITY) ? 0.f : ex2((mref - m) * L2E);
+      const float a_ot = (mo == -INFINITY) ? 0.f : ex2((mo - m) * L2E);
+      const float a0 = w == 0 ? a_me : a_ot, a1 = w == 0 ? a_ot : a_me;
       if (lane == 0 && wq == 0 && w == 0) ZG_TR(k, 13);
-      mbar_wait(&o_last[k & 1], (k >> 1) & 1);  // per buffer: a one-chunk next item cannot overtake it
+      mbar_wait(o_last, k & 1);  // the item's last PVs of both halves
       if (lane == 0 && wq == 0 && w == 0) ZG_TR(k, 14);
       tc_fence_after();
-      float inv;
-      {
-        uint32_t l1;
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(l1) : "r"(o_addr + DH));
-        tmem_ld_wait();
-        inv = 1.0f / __uint_as_float(l1);
+      const uint32_t o0 = tmem + TM_O + lane_off, o1 = o0 + TM_OS;
+      uint32_t l01[2];
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(l01[0]) : "r"(o0 + DH));
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(l01[1]) : "r"(o1 + DH));
+      uint32_t va[OH], vb[OH];
+      ld_cols(o0 + w * OH, va);
+      ld_cols(o1 + w * OH, vb);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(o_free);  // O_0 / O_1 are in registers: the next item's PVs may start
+      const float l = a0 * __uint_as_float(l01[0]) + a1 * __uint_as_float(l01[1]);
+      const float s0 = a0 / l, s1 = a1 / l;
+      uint4 pk[NQ];
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        float f[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          f[e] = __uint_as_float(va[8 * q + e]) * s0 + __uint_as_float(vb[8 * q + e]) * s1;
+        pk[q] = make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
       }
       if (P.tma_out) {
         // O tile -> shared memory (the TMA SW128 / SW32 layout of a [128, 64] + [128, 16] box) ->
         // one TMA tensor store per item: the stores leave through the async proxy instead of
         // 16-byte LSU stores to 128 scattered rows, which held this warp for ~3000 cycles
-        constexpr int NQ = OH / 8;  // 16-byte pieces of this half row
-        uint32_t a[32], a8[8];
-        tmem_ld32(o_addr + w * OH, a);
-        if constexpr (OH == 40)
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                       : "=r"(a8[0]), "=r"(a8[1]), "=r"(a8[2]), "=r"(a8[3]), "=r"(a8[4]), "=r"(a8[5]),
-                         "=r"(a8[6]), "=r"(a8[7])
-                       : "r"(o_addr + w * OH + 32));
-        tmem_ld_wait();
-        uint4 pk[NQ];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) pk[q] = scale_pack8(q < 4 ? a + 8 * q : a8, inv);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(o_free_k);  // O is in registers: the next item's PV may start
         const bool issuer = warp == 4 && lane == 0;
         if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
         named_bar_sync(6, 256);
@@ -642,47 +632,23 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
                          : "memory");
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
-        if (lane == 0 && wq == 0) ZG_TR(k, 4 + w);
-        return;
-      }
-      bool valid = row < P.S;
-      long long orow_off = (long long)u * P.o_unit_stride + (long long)row * P.ldo;
-      if (valid && P.o_rows) {
-        const int m = P.o_rows[(long long)u * P.S + row];
-        valid = m >= 0;
-        orow_off = (long long)m * P.ldo;
-      }
-      __nv_bfloat16* dst = P.out + orow_off + h * DH + w * OH;
-      {
-        uint32_t a[32];
-        tmem_ld32(o_addr + w * OH, a);
-        if constexpr (OH == 40) {
-          uint32_t a8[8];
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                       : "=r"(a8[0]), "=r"(a8[1]), "=r"(a8[2]), "=r"(a8[3]), "=r"(a8[4]), "=r"(a8[5]),
-                         "=r"(a8[6]), "=r"(a8[7])
-                       : "r"(o_addr + w * OH + 32));
-          tmem_ld_wait();
-          if (valid) {
-            uint4* d4 = reinterpret_cast<uint4*>(dst);  // 80-byte aligned row halves: 16-byte stores
+      } else {
+        bool valid = row < P.S;
+        long long orow_off = (long long)u * P.o_unit_stride + (long long)row * P.ldo;
+        if (valid && P.o_rows) {
+          const int mrow = P.o_rows[(long long)u * P.S + row];
+          valid = mrow >= 0;
+          orow_off = (long long)mrow * P.ldo;
+        }
+        if (valid) {
+          uint4* d4 = reinterpret_cast<uint4*>(P.out + orow_off + h * DH + w * OH);  // 16-byte aligned
 #pragma unroll
-            for (int q = 0; q < 4; ++q) d4[q] = scale_pack8(a + 8 * q, inv);
-            d4[4] = scale_pack8(a8, inv);
-          }
-        } else {
-          tmem_ld_wait();
-          if (valid) {
-            uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) d4[q] = scale_pack8(a + 8 * q, inv);
-          }
+          for (int q = 0; q < NQ; ++q) d4[q] = pk[q];
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(o_free_k);
       if (lane == 0 && wq == 0) ZG_TR(k, 4 + w);
     };
+
     const int G = gridDim.x;
     uint4 bqx[8];
     load_bq(blockIdx.x, load_sp(blockIdx.x), bqx);
@@ -691,10 +657,10 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     int sp_nn = load_sp(blockIdx.x + 2 * G);                  // and the row index of the one after
     int k = 0, c = 0;
     int kp = -1, ip = 0, hp = 0, up = 0;  // the previous item, whose epilogue is pending
+    float mp = -INFINITY;
     for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
       const int i = it % nmb, uh = it / nmb, h = uh % P.heads, u = uh / P.heads;
       const int nc = n_chunks(P, i);
-      o_addr = tmem + TM_O + (k & 1) * TM_OS + lane_off;
       if (lane == 0 && wq == 0) ZG_TR(k, 2 + w);
       float m_ref = -INFINITY;
       for (int j = 0; j < nc; ++j, ++c) {
@@ -722,61 +688,53 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
           for (int jj = 0; jj < 64; ++jj)
             if (jj >= kvalid) sr[jj] = __float_as_uint(-INFINITY);
         }
-        // P of this half's 64 keys against reference mref -> TMEM columns [64w, 64w + 32) (the half's
-        // own S columns, already in registers: no hazard with the partner half)
-        auto emit = [&](float mref) {
-          const float mc = (mref == -INFINITY) ? 0.f : mref * L2E;
-          const unsigned long long c2 = f32x2(cexp, cexp), m2 = f32x2(-mc, -mc);
-#pragma unroll
-          for (int g = 0; g < 2; ++g) {
-            uint32_t pk[16];
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              pk[q] = exp2_pair_bf16_ns(__uint_as_float(sr[32 * g + 2 * q]), __uint_as_float(sr[32 * g + 2 * q + 1]),
-                                        c2, m2);
-            }
-            tmem_st16(s_addr + 64 * w + 16 * g, pk);  // P (bf16) of keys [64w + 32g, +32)
-          }
-        };
         float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
         for (int jj = 0; jj < 64; jj += 4) {
           m0 = max3f(m0, __uint_as_float(sr[jj]), __uint_as_float(sr[jj + 1]));
           m1 = max3f(m1, __uint_as_float(sr[jj + 2]), __uint_as_float(sr[jj + 3]));
         }
-        // partial max -> partner half
-        const float mp = fmaxf(m0, m1);
-        xch[(buf * 2 + w) * BQ + r] = mp;
-        named_bar_sync(pair_bar, 64);
-        const float mx = tau * fmaxf(mp, xch[(buf * 2 + (w ^ 1)) * BQ + r]);  // row max logit
-        // lazy rescale (identical decision in both halves): a warp-wide TMEM round trip when any
-        // row of the warp moves its reference, alpha = 1 for the others
+        const float mx = tau * fmaxf(m0, m1);  // this half's row max logit
+        // lazy rescale of O_w: a warp-wide TMEM round trip when any row of the warp moves its
+        // reference, alpha = 1 for the others
         float alpha = 1.f;
         const bool upd = mx > m_ref + kThr || (m_ref == -INFINITY && mx > -INFINITY);
         if (upd) alpha = (m_ref == -INFINITY) ? 0.f : ex2((m_ref - mx) * L2E);
         if (__any_sync(0xffffffffu, upd)) {
           if (j > 0) {
-            mbar_wait(o_full, (c - 1) & 1);  // PV(c - 1) complete before O is rescaled
+            mbar_wait(&o_full[w], (c - 1) & 1);  // PV_w(c - 1) complete before O_w is rescaled
             tc_fence_after();
             o_scale(alpha);
           }
           if (upd) m_ref = mx;
         }
-        emit(m_ref);
+        {  // P of this half's 64 keys -> TMEM columns [64w, 64w + 32) (its own S columns)
+          const float mc = (m_ref == -INFINITY) ? 0.f : m_ref * L2E;
+          const unsigned long long c2 = f32x2(cexp, cexp), m2 = f32x2(-mc, -mc);
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+              pk[q] = exp2_pair_bf16_ns(__uint_as_float(sr[32 * g + 2 * q]), __uint_as_float(sr[32 * g + 2 * q + 1]),
+                                        c2, m2);
+            tmem_st16(s_addr + 64 * w + 16 * g, pk);
+          }
+        }
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[buf]);
+        if (lane == 0) mbar_arrive(&p_full[2 * buf + w]);
         if (lane == 0 && wq == 0 && j == 0 && w == 0) ZG_TR(k, 1);
         if (lane == 0 && wq == 0 && w == 0) ZG_T2(k, j, 2);
         if (j == 0 && kp >= 0) {
-          epilogue(kp, ip, hp, up);
+          epilogue(kp, ip, hp, up, mp);
           kp = -1;
         }
       }
-      kp = k, ip = i, hp = h, up = u;
+      kp = k, ip = i, hp = h, up = u, mp = m_ref;
     }
-    if (kp >= 0) epilogue(kp, ip, hp, up);
+    if (kp >= 0) epilogue(kp, ip, hp, up, mp);
   }
   if (P.tma_out && warp == 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
