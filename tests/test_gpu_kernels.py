@@ -51,9 +51,10 @@ def test_gemm_gelu_epilogue():
     assert rel(y, ref) < 5e-3
 
 
-def test_gemm_residual_scatter_zero_rows_and_device_m():
+@pytest.mark.parametrize("K_", [512, 2560])  # 2560: the TMA gather4 / scatter4 residual epilogue (long K)
+def test_gemm_residual_scatter_zero_rows_and_device_m(K_):
     g = torch.Generator(device=DEV).manual_seed(4)
-    M, N, K_ = 333, 768, 512
+    M, N = 333, 768
     a = torch.randn(M, K_, device=DEV, generator=g).bfloat16()
     w = (torch.randn(N, K_, device=DEV, generator=g) / 20).bfloat16()
     b = torch.randn(N, device=DEV, generator=g)
@@ -74,10 +75,31 @@ def test_gemm_residual_scatter_zero_rows_and_device_m():
     assert torch.equal(x[untouched], x0[untouched])
 
 
-def test_gemm_residual_modulo_rows():
+def test_gemm_residual_scatter_many_tiles_long_k():
+    """fc2-shaped residual scatter-add (K = 4C, many tiles per cluster: the TMA epilogue gathers the
+    next tile's rows while storing this one's), ragged M, bias."""
+    g = torch.Generator(device=DEV).manual_seed(14)
+    M, N, K_ = 20011, 1280, 5120
+    a = torch.randn(M, K_, device=DEV, generator=g).bfloat16()
+    w = (torch.randn(N, K_, device=DEV, generator=g) / 72).bfloat16()
+    b = torch.randn(N, device=DEV, generator=g)
+    x = torch.randn(25000, N, device=DEV, generator=g)
+    x0 = x.clone()
+    rm = torch.randperm(25000, device=DEV, generator=g)[:M].int()
+    K.gemm(a, w, b, epi=K.EPI_F32_RESID, out=x, res=x, row_map=rm)
+    ref = x0.clone()
+    ref[rm.long()] = x0[rm.long()] + a.float() @ w.float().T + b
+    assert rel(x, ref) < 1e-5
+    untouched = torch.ones(25000, dtype=torch.bool, device=DEV)
+    untouched[rm.long()] = False
+    assert torch.equal(x[untouched], x0[untouched])
+
+
+@pytest.mark.parametrize("K_", [256, 2560])
+def test_gemm_residual_modulo_rows(K_):
     g = torch.Generator(device=DEV).manual_seed(5)
-    a = torch.randn(3 * 64, 256, device=DEV, generator=g).bfloat16()
-    w = (torch.randn(256, 256, device=DEV, generator=g) / 16).bfloat16()
+    a = torch.randn(3 * 64, K_, device=DEV, generator=g).bfloat16()
+    w = (torch.randn(256, K_, device=DEV, generator=g) / (K_ ** 0.5)).bfloat16()
     pos = torch.randn(64, 256, device=DEV, generator=g)
     y = K.gemm(a, w, None, epi=K.EPI_F32_RESID, res=pos, res_mod=64)
     ref = a.float() @ w.float().T + pos.repeat(3, 1)

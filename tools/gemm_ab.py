@@ -1,5 +1,6 @@
 """A/B timing of zs_gemm_bf16 from two library builds (same box, interleaved): ViT-H shapes."""
 import ctypes
+import os
 import sys
 from pathlib import Path
 
@@ -9,7 +10,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2605_17633_b200 import _lib  # noqa: E402
 
 libs = {name: ctypes.CDLL(str(Path(_lib.LIB_PATH).parent / f)) for name, f in
-        [("new", "libzstripe_b200.so"), ("old", "libzstripe_b200_old.so")]}
+        [("new", os.environ.get("ZS_AB_NEW", "libzstripe_b200.so")), ("old", "libzstripe_b200_old.so")]}
 for l in libs.values():
     l.zs_gemm_bf16.argtypes = _lib.SIGNATURES["zs_gemm_bf16"]
 dev = "cuda"
