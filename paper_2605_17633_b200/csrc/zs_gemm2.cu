@@ -295,13 +295,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     };
-    auto buffer_read = [&](int pending) {  // this warp's stores older than the last `pending` have read smem
-      if (lane < 8) {
-        if (pending == 0)
-          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        else
-          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-      }
+    auto buffer_read = [&]() {  // this warp's stores have read their smem
+      if (lane < 8) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       __syncwarp();
     };
     constexpr int NCH = (BN / 2) / 32;  // chunks per tile half
@@ -362,16 +357,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
         }
         scatter(t, 32 * c, sr, b);
         // refill: the buffer whose store has been read gets the chunk kRB after the one it held
-        // (this tile's, or the next tile's first ones).  ZS_G2_LAZY: wait only for the previous
-        // chunk's store, so this chunk's store overlaps the next compute.
-#ifdef ZS_G2_LAZY
-        if (gc == 0) continue;
-        const int tgt = c - 1 + kRB, fb = (gc - 1) % kRB;
-        buffer_read(1);
-#else
+        // (this tile's, or the next tile's first ones)
         const int tgt = c + kRB, fb = b;
-        buffer_read(0);
-#endif
+        buffer_read();
         if (tgt < NCH)
           gather(t, 32 * tgt, lr, fb);
         else if (t + ncl < num_tiles)
@@ -608,8 +596,9 @@ int launch_gemm2(int epi, const void* A, long long lda, const void* W, long long
   // Rows are addressed by coordinate, so the row extent is left open (2^30) and only
   // coordinates the kernel computes from row_map / M are ever touched.
   static const bool g2_lsu = getenv("ZS_G2_LSU") != nullptr;  // A/B: force the LSU residual epilogue
+  static const bool g2_tma_all = getenv("ZS_G2_TMA_ALL") != nullptr;  // A/B: TMA epilogue at any K
   CUtensorMap tr = ta, to = ta;
-  if (epi == 2 && K >= 2560 && ep.res && ep.out && !(reinterpret_cast<uintptr_t>(ep.res) & 15) &&
+  if (epi == 2 && (K >= 2560 || g2_tma_all) && ep.res && ep.out && !(reinterpret_cast<uintptr_t>(ep.res) & 15) &&
       !(reinterpret_cast<uintptr_t>(ep.out) & 15) && !(ep.ld_res & 3) && !(ep.ld_out & 3) && !g2_lsu &&
       make_tmap_2d_f32(&tr, ep.res, (uint64_t)N, 1ull << 30, (uint64_t)ep.ld_res, 32, 1, CU_TENSOR_MAP_SWIZZLE_128B) == 0 &&
       make_tmap_2d_f32(&to, ep.out, (uint64_t)N, 1ull << 30, (uint64_t)ep.ld_out, 32, 1, CU_TENSOR_MAP_SWIZZLE_128B) == 0)
