@@ -53,20 +53,6 @@ int make_tmap_2d_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t 
   return r == CUDA_SUCCESS ? 0 : ZS_ERR_TMAP;
 }
 
-int make_tmap_2d_f32(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
-                     uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz) {
-  auto fn = encode_fn();
-  if (!fn) return ZS_ERR_DEVICE;
-  cuuint64_t dims[2] = {inner, outer};
-  cuuint64_t strides[1] = {ld_elems * 4};
-  cuuint32_t box[2] = {box_inner, box_outer};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? 0 : ZS_ERR_TMAP;
-}
-
 int make_tmap_3d_bf16(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t ld1_elems,
                       uint64_t ld2_elems, uint32_t b0, uint32_t b1, uint32_t b2, CUtensorMapSwizzle swz) {
   auto fn = encode_fn();

@@ -27,23 +27,6 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int XS = 36;                                   // padded row stride (floats) of the epilogue transpose
 constexpr int EPI_SMEM = 8 * 32 * XS * 4;                // per epilogue warp: 32 rows x 32 fp32
 constexpr int SMEM_BYTES = kStages * STAGE_BYTES + 256 + EPI_SMEM + 1024;
-// EPI 3 (fp32 residual through TMA): per epilogue warp kRB buffers of one 32-row x 32-column
-// fp32 chunk (4 KB, SW128), gathered / scattered four rows per TMA instruction
-#ifndef ZS_G2_RB
-#define ZS_G2_RB 2
-#endif
-constexpr int kRB = ZS_G2_RB;
-constexpr int RB_BYTES = 32 * 32 * 4;
-#ifndef ZS_G2_DEAD
-#define ZS_G2_DEAD (1 << 30)
-#endif
-constexpr int kDeadRow = ZS_G2_DEAD;  // row coordinate of rows past M: out of the maps' bounds
-#ifndef ZS_G2_STAGES3
-#define ZS_G2_STAGES3 5
-#endif
-constexpr int kStages3 = ZS_G2_STAGES3;  // operand ring of the EPI 3 kernel (shares smem with the buffers)
-constexpr int SMEM3_BYTES = kStages3 * STAGE_BYTES + 1024 + 8 * kRB * RB_BYTES + 1024;
-static_assert(SMEM3_BYTES <= 232448, "EPI 3 shared memory");
 constexpr int kThreads = 384;
 constexpr int kEpiThreads = 256;
 constexpr uint32_t kTmemCols = 2 * BN;  // two accumulators
@@ -132,20 +115,18 @@ __device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols
 
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
-    zs_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmR, const __grid_constant__ CUtensorMap tmO, int M, int N,
+    zs_gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int K, GemmEpi ep) {
   using namespace gemm2;
-  constexpr int NST = EPI == 3 ? kStages3 : kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * STAGE_BYTES);
-  uint64_t* full = bars;                       // [NST]  (leader: 2 arrivals + tx)
-  uint64_t* empty = bars + NST;            // [NST]  (multicast commit)
-  uint64_t* tfull = bars + 2 * NST;        // [2]        (multicast commit)
-  uint64_t* tempty = bars + 2 * NST + 2;   // [2]        (leader: 2 x 256 epilogue threads)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * NST + 4);
-  float* xstage = reinterpret_cast<float*>(smem + NST * STAGE_BYTES + 256);  // [8 warps][32][XS]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * STAGE_BYTES);
+  uint64_t* full = bars;                       // [kStages]  (leader: 2 arrivals + tx)
+  uint64_t* empty = bars + kStages;            // [kStages]  (multicast commit)
+  uint64_t* tfull = bars + 2 * kStages;        // [2]        (multicast commit)
+  uint64_t* tempty = bars + 2 * kStages + 2;   // [2]        (leader: 2 x 256 epilogue threads)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  float* xstage = reinterpret_cast<float*>(smem + kStages * STAGE_BYTES + 256);  // [8 warps][32][XS]
 
   // warp index via shfl: provably warp-uniform, so role code can use uniform registers
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -155,12 +136,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    if constexpr (EPI == 3) {
-      tma_prefetch_desc(&tmR);
-      tma_prefetch_desc(&tmO);
-      for (int s = 0; s < 8 * kRB; ++s) mbar_init(bars + 16 + s, 1);
-    }
-    for (int s = 0; s < NST; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 2);
       mbar_init(&empty[s], 1);
     }
@@ -200,7 +176,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
             mbar_arrive_remote(&full[stage], 0);
           tma_load_2d_pair(sa, &tmA, &full[stage], kb * BK, m0);
           tma_load_2d_pair(sb, &tmB, &full[stage], kb * BK, n0);
-          if (++stage == NST) {
+          if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
@@ -231,145 +207,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(gemm2::kThreads, 1)
           for (int k = 0; k < BK / UK; ++k) umma_pair_elect(dtm, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
           umma_commit_pair_elect(&empty[stage]);
           if (kb == nk - 1) umma_commit_pair_elect(&tfull[as]);
-          if (++stage == NST) {
+          if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
     }
-  } else if (EPI == 3 && warp >= 4) {
-    // fp32 residual stream: out[orow] = acc + bias + res[rrow] with the rows moved by TMA.
-    // Each warp owns 32 rows x one 128-column half of the tile, in four 32-column chunks that
-    // rotate through kRB shared-memory buffers: gather4 loads (4 residual rows per instruction,
-    // lanes 0-7 one group each) are issued as soon as a buffer's previous scatter4 store has
-    // been read, and the first chunks of the next tile are gathered while this tile's last
-    // chunks are stored, so residual reads run ahead of the accumulator instead of behind it.
-    // Thread = row: lane r reads / writes its row's 16-byte pieces at (j ^ (r & 7)) (SW128),
-    // conflict-free.  Rows past M use coordinate kDeadRow (TMA out of bounds: zero-filled loads,
-    // skipped stores); zero_rows rows store zeros without loading.
-    const int ew = warp - 4, q = warp & 3, chalf = ew >> 2;
-    uint8_t* rb = smem + NST * STAGE_BYTES + 1024 + ew * kRB * RB_BYTES;
-    uint64_t* rbar = bars + 16 + ew * kRB;
-    uint32_t rphase = 0;  // bit b: parity of buffer b's next completion
-    auto ld_row_v = [&](const int* p) {
-      int v;
-      asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-      return v;
-    };
-    auto rows_of = [&](int tt, int& lr, int& sr, int& z) {
-      lr = sr = kDeadRow;
-      z = 0;
-      if (tt >= num_tiles) return;
-      const int m = (tt / n_tiles) * 2 * BM + rank * BM + q * 32 + lane;
-      if (m >= M) return;
-      sr = ep.row_map ? ld_row_v(ep.row_map + m) : m;
-      z = ep.zero_rows ? (int)ep.zero_rows[m] : 0;
-      lr = z ? kDeadRow : (ep.res_mod > 0 ? m % ep.res_mod : sr);
-    };
-    auto gather = [&](int tt, int c, int lr, int b) {  // chunk c (column offset) of tile tt -> buffer b
-      const int col = (tt % n_tiles) * BN + chalf * (BN / 2) + c, g = lane & 7;
-      const int r0 = __shfl_sync(0xffffffffu, lr, 4 * g), r1 = __shfl_sync(0xffffffffu, lr, 4 * g + 1);
-      const int r2 = __shfl_sync(0xffffffffu, lr, 4 * g + 2), r3 = __shfl_sync(0xffffffffu, lr, 4 * g + 3);
-      if (lane == 0) mbar_expect_tx(&rbar[b], RB_BYTES);
-      __syncwarp();
-      if (lane < 8)
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-            " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(rb + b * RB_BYTES + g * 512)),
-            "l"(reinterpret_cast<uint64_t>(&tmR)), "r"(smem_u32(&rbar[b])), "r"(col), "r"(r0), "r"(r1), "r"(r2),
-            "r"(r3)
-            : "memory");
-    };
-    auto scatter = [&](int tt, int c, int sr, int b) {  // buffer b -> chunk c of tile tt, then buffer free
-      const int col = (tt % n_tiles) * BN + chalf * (BN / 2) + c, g = lane & 7;
-      const int r0 = __shfl_sync(0xffffffffu, sr, 4 * g), r1 = __shfl_sync(0xffffffffu, sr, 4 * g + 1);
-      const int r2 = __shfl_sync(0xffffffffu, sr, 4 * g + 2), r3 = __shfl_sync(0xffffffffu, sr, 4 * g + 3);
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane < 8) {
-        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];"
-                     ::"l"(reinterpret_cast<uint64_t>(&tmO)), "r"(smem_u32(rb + b * RB_BYTES + g * 512)), "r"(col),
-                     "r"(r0), "r"(r1), "r"(r2), "r"(r3)
-                     : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-    };
-    auto buffer_read = [&]() {  // this warp's stores have read their smem
-      if (lane < 8) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      __syncwarp();
-    };
-    constexpr int NCH = (BN / 2) / 32;  // chunks per tile half
-    static_assert(kRB >= 2 && kRB <= NCH, "EPI 3 buffer count");
-    int lr, sr, z;
-    rows_of(cid, lr, sr, z);
-    int it = 0, gc = 0;  // gc: chunks completed by this warp (buffer gc % kRB)
-    for (int c = 0; c < kRB; ++c) gather(cid, 32 * c, lr, c);
-    for (int t = cid; t < num_tiles; t += ncl, ++it) {
-      const int as = it & 1;
-      int nlr, nsr, nz;
-      rows_of(t + ncl, nlr, nsr, nz);
-      if (nlr != kDeadRow) {  // L2 prefetch of the next tile's residual half row (the later chunks' gathers hit L2)
-        const int pn0 = ((t + ncl) % n_tiles) * BN + chalf * (BN / 2);
-        const int ncols = min(BN / 2, N - pn0);
-        if (ncols > 0)
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ep.res + (long long)nlr * ep.ld_res + pn0),
-                       "r"(ncols * 4)
-                       : "memory");
-      }
-      mbar_wait_sleep(&tfull[as], (it >> 1) & 1);
-      tc_fence_after();
-      const uint32_t trow = tmem_base + as * BN + ((uint32_t)(q * 32) << 16) + chalf * (BN / 2);
-      const int nbase = (t % n_tiles) * BN + chalf * (BN / 2);
-#pragma unroll 1
-      for (int c = 0; c < NCH; ++c, ++gc) {
-        const int b = gc % kRB;
-        uint32_t r[32];
-        __syncwarp();
-        tmem_ld32(trow + 32 * c, r);
-        tmem_ld_wait();
-        if (c == NCH - 1) {  // accumulator drained: release it to the MMA warp
-          tc_fence_before();
-          if (leader)
-            mbar_arrive(&tempty[as]);
-          else
-            mbar_arrive_remote(&tempty[as], 0);
-        }
-        mbar_wait(&rbar[b], (rphase >> b) & 1);
-        rphase ^= 1u << b;
-        const int nb = nbase + 32 * c;
-        float4* row = reinterpret_cast<float4*>(rb + b * RB_BYTES + lane * 128);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float4 bj = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (ep.bias && nb < N) bj = __ldg(reinterpret_cast<const float4*>(ep.bias + nb) + j);
-          float4* p = row + (j ^ (lane & 7));
-          float4 a = *p;
-          if (z) {
-            a = make_float4(0.f, 0.f, 0.f, 0.f);
-          } else {
-            a.x += __uint_as_float(r[4 * j]) + bj.x;
-            a.y += __uint_as_float(r[4 * j + 1]) + bj.y;
-            a.z += __uint_as_float(r[4 * j + 2]) + bj.z;
-            a.w += __uint_as_float(r[4 * j + 3]) + bj.w;
-          }
-          *p = a;
-        }
-        scatter(t, 32 * c, sr, b);
-        // refill: the buffer whose store has been read gets the chunk kRB after the one it held
-        // (this tile's, or the next tile's first ones)
-        const int tgt = c + kRB, fb = b;
-        buffer_read();
-        if (tgt < NCH)
-          gather(t, 32 * tgt, lr, fb);
-        else if (t + ncl < num_tiles)
-          gather(t + ncl, 32 * (tgt - NCH), nlr, fb);
-      }
-      lr = nlr;
-      sr = nsr;
-      z = nz;
-    }
-    if (lane < 8) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else if (warp >= 4) {
     const int ew = warp - 4;
     const int q = warp & 3;          // TMEM lane quarter
@@ -589,36 +433,18 @@ int launch_gemm2(int epi, const void* A, long long lda, const void* W, long long
   const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
   int grid = (num_sms() / 2) * 2;
   if (grid > 2 * tiles) grid = 2 * tiles;
-  // fp32 residual epilogue through TMA gather4 / scatter4 (EPI 3) for long-K GEMMs (fc2, K = 4C)
-  // when both row arrays qualify (16-byte aligned base and row pitch).  Paired A/B on ViT-H
-  // shapes (tools/gemm_ab.py): fc2 -3 to -8 %, but proj (K = C: a short mainloop per tile)
-  // +9 to +32 % for every buffer / stage split tried, so short-K GEMMs keep the LSU epilogue.
-  // Rows are addressed by coordinate, so the row extent is left open (2^30) and only
-  // coordinates the kernel computes from row_map / M are ever touched.
-  static const bool g2_lsu = getenv("ZS_G2_LSU") != nullptr;  // A/B: force the LSU residual epilogue
-  static const bool g2_tma_all = getenv("ZS_G2_TMA_ALL") != nullptr;  // A/B: TMA epilogue at any K
-  CUtensorMap tr = ta, to = ta;
-  if (epi == 2 && (K >= 2560 || g2_tma_all) && ep.res && ep.out && !(reinterpret_cast<uintptr_t>(ep.res) & 15) &&
-      !(reinterpret_cast<uintptr_t>(ep.out) & 15) && !(ep.ld_res & 3) && !(ep.ld_out & 3) && !g2_lsu &&
-      make_tmap_2d_f32(&tr, ep.res, (uint64_t)N, 1ull << 30, (uint64_t)ep.ld_res, 32, 1, CU_TENSOR_MAP_SWIZZLE_128B) == 0 &&
-      make_tmap_2d_f32(&to, ep.out, (uint64_t)N, 1ull << 30, (uint64_t)ep.ld_out, 32, 1, CU_TENSOR_MAP_SWIZZLE_128B) == 0)
-    epi = 3;
   switch (epi) {
     case 0:
       cudaFuncSetAttribute(zs_gemm2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-      { zs_gemm2_kernel<0><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, tr, to, M, N, K, ep); count_launch(); }
+      { zs_gemm2_kernel<0><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep); count_launch(); }
       break;
     case 1:
       cudaFuncSetAttribute(zs_gemm2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-      { zs_gemm2_kernel<1><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, tr, to, M, N, K, ep); count_launch(); }
+      { zs_gemm2_kernel<1><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep); count_launch(); }
       break;
     case 2:
       cudaFuncSetAttribute(zs_gemm2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-      { zs_gemm2_kernel<2><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, tr, to, M, N, K, ep); count_launch(); }
-      break;
-    case 3:
-      cudaFuncSetAttribute(zs_gemm2_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3_BYTES);
-      { zs_gemm2_kernel<3><<<grid, kThreads, SMEM3_BYTES, stream>>>(ta, tb, tr, to, M, N, K, ep); count_launch(); }
+      { zs_gemm2_kernel<2><<<grid, kThreads, SMEM_BYTES, stream>>>(ta, tb, M, N, K, ep); count_launch(); }
       break;
     default:
       return ZS_ERR_ARG;

@@ -33,9 +33,6 @@ int num_sms();
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 int make_tmap_2d_bf16(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
                       uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz);
-// fp32 rows (the residual-stream epilogue's gather4 / scatter4 maps)
-int make_tmap_2d_f32(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld_elems,
-                     uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle swz);
 int make_tmap_3d_bf16(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t ld1_elems,
                       uint64_t ld2_elems, uint32_t b0, uint32_t b1, uint32_t b2, CUtensorMapSwizzle swz);
 
