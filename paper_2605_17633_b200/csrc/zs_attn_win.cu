@@ -57,7 +57,7 @@ struct Params {
   int kv_rows;  // rows of the K/V slabs
   // smem layout (byte offsets from the 1024-aligned base; buffer b adds b * buf_bytes)
   int off_qa, off_k, off_qb, off_v, off_qa_t, off_k_t, off_qb_t, off_v_t, buf_bytes;
-  int off_bq_h, off_bq_w, off_kb_h, off_kb_w, off_bar;
+  int off_kb_h, off_kb_w, kb_buf, off_bar;  // one-hot key rows: two buffers kb_buf bytes apart
   int tx_qk, tx_v;
   // schedule
   unsigned char live[8];  // per softmax warp (tile*4 + w): bit g = key group g live
@@ -67,6 +67,7 @@ struct Params {
   int nrun[2];
   short run_k0[2][kMaxRuns], run_n[2][kMaxRuns], run_c0[2][kMaxRuns];  // key start, length, S column
   int s_col[2], o_col[2];                                               // TMEM column bases
+  int tm_bq;                                                            // TMEM: Bq rows, 16 columns per tile
   __nv_bfloat16* out;
   int trace;
 };
@@ -79,16 +80,6 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
-}
-// D[tmem] (+)= A[tmem] * B[smem]: A (P, bf16, K-major) read from tensor memory.
-__device__ __forceinline__ void umma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                                             uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
 }
 // fp16 x fp16 -> fp32 instruction descriptor (A/B K-major)
 __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
@@ -229,8 +220,9 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
   uint64_t* s_full = bar + 8;     // [tile]
   uint64_t* p_full = bar + 10;    // [tile]   live softmax warps: P written, O of the previous item read
   uint64_t* o_full = bar + 12;    // [tile]
-  uint64_t* bk_full = bar + 14;   // bias operands (Bq rows, one-hot K rows) of the item in smem
-  uint64_t* bk_empty = bar + 15;  // S MMAs that read them completed
+  uint64_t* bk_full = bar + 14;   // [2] one-hot key rows of the item in smem buffer k & 1 (warps 2, 3)
+  uint64_t* bk_empty = bar + 16;  // [2] S MMAs that read that buffer completed
+  uint64_t* bq_full = bar + 18;   // [tile] live softmax warps: the item's Bq rows are in TMEM
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 20);
 
   // warp index via shfl: provably warp-uniform, so role code can use uniform registers
@@ -251,8 +243,11 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
       mbar_init(&p_full[s], (uint32_t)max(1, min(4, (P.S - 128 * s + 31) / 32)));
       mbar_init(&o_full[s], 1);
     }
-    mbar_init(bk_full, 2);
-    mbar_init(bk_empty, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bk_full[s], 2);
+      mbar_init(&bk_empty[s], 1);
+      mbar_init(&bq_full[s], (uint32_t)max(1, min(4, (P.S - 128 * s + 31) / 32)));
+    }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
@@ -309,13 +304,14 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
       const uint64_t dq[2] = {sdesc_k_sw128(smem + P.off_qa), sdesc_k_sw128(smem + P.off_qb)};
       const uint64_t dqt[2] = {sdesc_k_sw32(smem + P.off_qa_t), sdesc_k_sw32(smem + P.off_qb_t)};
       const uint64_t dk = sdesc_k_sw128(smem + P.off_k), dkt = sdesc_k_sw32(smem + P.off_k_t);
-      const uint64_t dbh = sdesc_k_sw32(smem + P.off_bq_h), dbw = sdesc_k_sw32(smem + P.off_bq_w);
       const uint64_t dkh = sdesc_k_sw32(smem + P.off_kb_h), dkw = sdesc_k_sw32(smem + P.off_kb_w);
+      const uint32_t kbd = (uint32_t)P.kb_buf >> 4;
       const uint64_t dv = sdesc_mn_sw128(smem + P.off_v), dvt = sdesc_mn_sw32(smem + P.off_v_t);
       auto issue_s = [&](int X, int b) {
         const uint64_t q = dq[X] + b * bufd, qt = dqt[X] + b * bufd;
         const uint64_t kk = dk + b * bufd, kt = dkt + b * bufd;
-        const uint64_t bh = dbh + X * 256, bw = dbw + X * 256;  // tile B rows start at row 128 (x32 B)
+        const uint64_t kh = dkh + b * kbd, kw = dkw + b * kbd;
+        const uint32_t bq = tmem + P.tm_bq + 16 * X;  // A operand: this tile's [bh | bw] rows (fp16)
         const uint32_t d0 = tmem + P.s_col[X];
         for (int r = 0; r < P.nrun[X]; ++r) {
           const int k0 = P.run_k0[X][r], n = P.run_n[X][r];
@@ -324,8 +320,8 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) umma_ss(d, q + 2 * ks, kk + k0 * 8 + 2 * ks, id, ks > 0);
           if constexpr (kTail) umma_ss(d, qt, kt + k0 * 2, id, 1);
-          umma_ss(d, bh, dkh + k0 * 2, idh, 1);  // + bh[σq, ky] / tau
-          umma_ss(d, bw, dkw + k0 * 2, idh, 1);  // + bw[σq, kx] / tau
+          umma_ts(d, bq, kh + k0 * 2, idh, 1);      // + bh[σq, ky] / tau
+          umma_ts(d, bq + 8, kw + k0 * 2, idh, 1);  // + bw[σq, kx] / tau
         }
         umma_commit_elect(&s_full[X]);
       };
@@ -354,16 +350,19 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
           const int b = k & 1;
           mbar_wait(&qk_full[b], (k >> 1) & 1);
-          mbar_wait(bk_full, k & 1);
+          mbar_wait(&bk_full[b], (k >> 1) & 1);
+          mbar_wait(&bq_full[0], k & 1);
           tc_fence_after();
           issue_s(0, b);
           mbar_wait_sleep(&p_full[0], k & 1);
           mbar_wait(&v_full[b], (k >> 1) & 1);
           tc_fence_after();
           issue_pv(0, b);
+          mbar_wait(&bq_full[1], k & 1);
+          tc_fence_after();
           issue_s(1, b);
           umma_commit_elect(&qk_empty[b]);
-          umma_commit_elect(bk_empty);
+          umma_commit_elect(&bk_empty[b]);
           mbar_wait_sleep(&p_full[1], k & 1);
           tc_fence_after();
           issue_pv(1, b);
@@ -373,7 +372,8 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
       for (int it = P.seq ? P.items : blockIdx.x; it < P.items; it += gridDim.x, ++k) {
         const int b = k & 1;
         mbar_wait(&qk_full[b], (k >> 1) & 1);
-        mbar_wait(bk_full, k & 1);
+        mbar_wait(&bk_full[b], (k >> 1) & 1);
+        mbar_wait(&bq_full[0], k & 1);
         tc_fence_after();
         issue_s(0, b);
         if (lane == 0) ZS_TR(k, 2);
@@ -385,11 +385,13 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
             umma_commit_elect(&v_empty[pb]);
             if (lane == 0) ZS_TR(k, 3);
           }
+          mbar_wait(&bq_full[1], k & 1);
+          tc_fence_after();
           issue_s(1, b);
           if (lane == 0) ZS_TR(k, 4);
         }
         umma_commit_elect(&qk_empty[b]);
-        umma_commit_elect(bk_empty);
+        umma_commit_elect(&bk_empty[b]);
         mbar_wait_sleep(&p_full[0], k & 1);
         mbar_wait(&v_full[b], (k >> 1) & 1);
         tc_fence_after();
@@ -405,45 +407,39 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         umma_commit_elect(&v_empty[pb]);
       }
     } else {
-      // ---------------------------------------------------------- bias operands of each item
-      //  warp 3 - Bq: fp16 rows btab[h, σq(r)] (two 16-column SW32 slabs bh | bw)
-      //  warp 2 - Kb: one-hot rows kb1[σk(j)] = e_{σk/w} | e_{σk%w}
-      // both 64-byte-row gathers with 16-byte cp.async (8 rows x 4 chunks per instruction)
-      const bool is_q = warp == 3;
-      const int nrows = is_q ? P.S : P.kv_rows;
-      const uint32_t off_h = is_q ? P.off_bq_h : P.off_kb_h, off_w = is_q ? P.off_bq_w : P.off_kb_w;
+      // ---------------------------------------------------------- one-hot key rows of each item
+      // kb1[σk(j)] = e_{σk/w} | e_{σk%w} (two 16-column SW32 slabs), 64-byte-row gathers with
+      // 16-byte cp.async (8 rows x 4 chunks per instruction); warp 2 rows [0, 128), warp 3 the
+      // rest, into buffer k & 1 — the item ahead is gathered while this item's S' runs
+      const int i0 = (warp - 2) * 4;
+      const int nrows = P.kv_rows;
       const int c = lane & 3;
-      uint8_t* slab = smem + ((c >> 1) ? off_w : off_h);
       int k = 0;
       for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
-        const int u = it / P.heads, h = it % P.heads;
-        const int* isrc = (is_q ? P.q_sp : P.k_sp) + (long long)u * P.S;
-        int idx[8];
+        const int u = it / P.heads, b = k & 1;
+        const int* isrc = P.k_sp + (long long)u * P.S;
+        uint8_t* slab = smem + ((c >> 1) ? P.off_kb_w : P.off_kb_h) + b * P.kb_buf;
+        int idx[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int j = lane + 32 * i;
+        for (int i = 0; i < 4; ++i) {
+          const int j = lane + 32 * (i0 + i);
           idx[i] = j < P.S ? __ldg(isrc + j) : -1;
         }
-        const __half* tab = is_q ? P.btab + (long long)u * P.btab_us + (long long)h * P.S * 32 : P.kb1;
-        mbar_wait_sleep(bk_empty, (k & 1) ^ 1);
+        mbar_wait_sleep(&bk_empty[b], ((k >> 1) & 1) ^ 1);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (32 * i >= nrows) break;
+        for (int i = 0; i < 4; ++i) {
+          if (32 * (i0 + i) >= nrows) break;
 #pragma unroll
           for (int l = 0; l < 32; l += 8) {
             const int rl = l + (lane >> 2);
-            const int r = 32 * i + rl;
+            const int r = 32 * (i0 + i) + rl;
             const int sp = __shfl_sync(0xffffffffu, idx[i], rl);
             if (r < nrows) {
               uint8_t* dst = slab + sw32_off(r, c & 1);
-#ifdef ZS_WIN_NOGATHER
-              if (false) {
-#else
-              if (sp >= 0) {
-#endif
-                cp_async16(dst, tab + (long long)sp * 32 + c * 8);
-              }
-              else *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);  // key rows past S
+              if (sp >= 0)
+                cp_async16(dst, P.kb1 + (long long)sp * 32 + c * 8);
+              else
+                *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);  // key rows past S
             }
           }
         }
@@ -451,8 +447,8 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         fence_proxy_async_smem();  // generic-proxy smem writes -> tensor core
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(bk_full);
-          if (is_q) ZS_TR(k, 8);
+          mbar_arrive(&bk_full[b]);
+          if (warp == 2) ZS_TR(k, 8);
         }
       }
     }
@@ -526,6 +522,51 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
       else group_emit<16>(sr, pa, cexp, mc, rs);
     };
 
+    // Bq rows (the A operand of the bias MMAs, 32 fp16 [bh | bw] / tau per query row) live in
+    // TMEM, written by the row's own thread: for item k + 1 as soon as S'(k) has completed (its
+    // last read of Bq(k)), from registers loaded one item ahead; the spatial index σq of the
+    // row one item before that.  Rows past S write zeros (their S' rows are never used).
+    const uint32_t bq_addr = tmem + P.tm_bq + 16 * X + lane_off;
+    const int G = gridDim.x;
+    auto load_sp = [&](int it2) -> int {
+      int v = -1;
+      if (valid && it2 < P.items)
+        asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(P.q_sp + (long long)(it2 / P.heads) * P.S + row) : "memory");
+      return v;
+    };
+    auto load_bq = [&](int it2, int sp, uint4 (&x)[4]) {
+      const int u2 = it2 / P.heads, h2 = it2 % P.heads;
+      const uint4* src = reinterpret_cast<const uint4*>(P.btab + (long long)u2 * P.btab_us + ((long long)h2 * P.S + sp) * 32);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        x[q] = make_uint4(0u, 0u, 0u, 0u);
+        if (sp >= 0 && it2 < P.items)
+          asm volatile("ld.global.nc.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(x[q].x), "=r"(x[q].y), "=r"(x[q].z), "=r"(x[q].w)
+                       : "l"(src + q)
+                       : "memory");
+      }
+    };
+    auto store_bq = [&](const uint4 (&x)[4]) {
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+          "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(bq_addr),
+          "r"(x[0].x), "r"(x[0].y), "r"(x[0].z), "r"(x[0].w), "r"(x[1].x), "r"(x[1].y), "r"(x[1].z), "r"(x[1].w),
+          "r"(x[2].x), "r"(x[2].y), "r"(x[2].z), "r"(x[2].w), "r"(x[3].x), "r"(x[3].y), "r"(x[3].z), "r"(x[3].w)
+          : "memory");
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bq_full[X]);
+    };
+    uint4 bqn[4];
+    int spn = -1;
+    if (warp_live && blockIdx.x < P.items) {
+      load_bq(blockIdx.x, load_sp(blockIdx.x), bqn);
+      store_bq(bqn);                                       // item 0
+      load_bq(blockIdx.x + G, load_sp(blockIdx.x + G), bqn);  // item 1, in flight during item 0
+      spn = load_sp(blockIdx.x + 2 * G);
+    }
     int k = 0;
     int prev_it = -1, prev_om = 0;
     float prev_inv = 0.f;
@@ -534,6 +575,11 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         const int om = out_row(it);
         mbar_wait(&s_full[X], k & 1);
         tc_fence_after();
+        if (it + G < P.items) {  // S'(k) done reading Bq(k): install Bq(k + 1)
+          store_bq(bqn);
+          load_bq(it + 2 * G, spn, bqn);
+          spn = load_sp(it + 3 * G);
+        }
         if (lane == 0) ZS_TR(k, 16 + 8 * X + 2);
         float mx = -INFINITY, rs = 0.f;
         if constexpr (REG) {
@@ -692,21 +738,23 @@ int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, 
   }
   const int wa = (p.s_col[0] + 31) & ~31, wb = p.s_col[1];
   p.seq = 0;
-  if (wa + wb + 2 * 80 > (int)kTmemCols) {
+  // TMEM: S columns | Bq (2 x 16) | O_A | O_B (96 wide when they fit, else 80)
+  if (wa + wb + 32 + 2 * 80 > (int)kTmemCols) {
     // high density: tiles A and B one after the other over shared S columns
-    if (p.nt < 2 || std::max(wa, wb) + 2 * 80 > (int)kTmemCols || getenv("ZS_WIN_NO_SEQ")) return 1;
+    if (p.nt < 2 || std::max(wa, wb) + 32 + 2 * 80 > (int)kTmemCols || getenv("ZS_WIN_NO_SEQ")) return 1;
     p.seq = 1;
   }
   p.s_col[0] = 0;
   p.s_col[1] = p.seq ? 0 : wa;
   const int s_cols = p.seq ? std::max(wa, wb) : wa + wb;
-  if (s_cols <= (int)kTmemCols - 2 * 96) {  // O accumulators 32-column aligned when they fit
+  if (s_cols + 32 <= (int)kTmemCols - 2 * 96) {  // O accumulators 32-column aligned when they fit
     p.o_col[0] = (int)kTmemCols - 2 * 96;
     p.o_col[1] = (int)kTmemCols - 96;
   } else {
     p.o_col[0] = (int)kTmemCols - 2 * 80;
     p.o_col[1] = (int)kTmemCols - 80;
   }
+  p.tm_bq = p.o_col[0] - 32;
   if (p.nrun[1] == 0) p.nt = 1;
   if (p.nt == 1) p.seq = 0;
   p.nlw = 0;
@@ -741,11 +789,11 @@ int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, 
   if (tail) off = std::max(off, p.off_qb_t + 128 * 32);
   p.buf_bytes = (off + 1023) / 1024 * 1024;
   off = 2 * p.buf_bytes;
-  // Bq slabs: tile A rows [0,128) then tile B rows (the MMA reads 128 rows from 128*32)
-  p.off_bq_h = take(256 * 32, 1024);
-  p.off_bq_w = take(256 * 32, 1024);
-  p.off_kb_h = take(kvs * 32, 256);
+  // one-hot key rows, two buffers: [kb_h | kb_w] of buffer 0, then of buffer 1
+  p.off_kb_h = take(kvs * 32, 1024);
   p.off_kb_w = take(kvs * 32, 256);
+  p.kb_buf = (off - p.off_kb_h + 1023) / 1024 * 1024;
+  off = p.off_kb_h + 2 * p.kb_buf;
   p.off_bar = take(256, 8);
   const size_t smem = 1024 + (size_t)off;
   if (smem > 227 * 1024) return 1;
