@@ -57,7 +57,7 @@ struct Params {
   int kv_rows;  // rows of the K/V slabs
   // smem layout (byte offsets from the 1024-aligned base; buffer b adds b * buf_bytes)
   int off_qa, off_k, off_qb, off_v, off_qa_t, off_k_t, off_qb_t, off_v_t, buf_bytes;
-  int off_kb_h, off_kb_w, kb_buf, off_bar;  // one-hot key rows: two buffers kb_buf bytes apart
+  int off_kb_h, off_kb_w, kb_buf, off_bar;  // one-hot key rows (TMEM-Bq variant: two buffers kb_buf bytes apart)
   int tx_qk, tx_v;
   // schedule
   unsigned char live[8];  // per softmax warp (tile*4 + w): bit g = key group g live
@@ -67,9 +67,10 @@ struct Params {
   int nrun[2];
   short run_k0[2][kMaxRuns], run_n[2][kMaxRuns], run_c0[2][kMaxRuns];  // key start, length, S column
   int s_col[2], o_col[2];                                               // TMEM column bases
-  int tm_bq;                                                            // TMEM: Bq rows, 16 columns per tile
+  int tm_bq;                                                            // TMEM: Bq rows, 16 columns per tile (BQT)
   __nv_bfloat16* out;
   int trace;
+  int off_bq_h, off_bq_w;  // Bq slabs (shared-memory Bq variant only)
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -199,7 +200,11 @@ __device__ unsigned long long g_win_trace[64 * 32];
 
 // REG: all live groups of a row fit in registers (<= 3 groups of 32); otherwise S' is
 // re-read from TMEM for the exp pass.
-template <int DH, bool REG>
+// BQT: the Bq rows live in TMEM (written by the softmax threads one item ahead) and the one-hot
+// key rows are double-buffered, so neither gather sits on the MMA chain.  Without BQT (when the
+// 32 TMEM columns do not fit next to S_A + S_B + O_A + O_B, e.g. d = 0.6 windows) warp 3 gathers
+// the Bq rows into shared-memory slabs and the key rows are single-buffered.
+template <int DH, bool REG, bool BQT>
 __global__ void __launch_bounds__(attnw::kThreads, 1)
     zs_attn_win_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tq_t,
                        const __grid_constant__ CUtensorMap tk, const __grid_constant__ CUtensorMap tk_t,
@@ -305,7 +310,8 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
       const uint64_t dqt[2] = {sdesc_k_sw32(smem + P.off_qa_t), sdesc_k_sw32(smem + P.off_qb_t)};
       const uint64_t dk = sdesc_k_sw128(smem + P.off_k), dkt = sdesc_k_sw32(smem + P.off_k_t);
       const uint64_t dkh = sdesc_k_sw32(smem + P.off_kb_h), dkw = sdesc_k_sw32(smem + P.off_kb_w);
-      const uint32_t kbd = (uint32_t)P.kb_buf >> 4;
+      const uint64_t dbh = sdesc_k_sw32(smem + P.off_bq_h), dbw = sdesc_k_sw32(smem + P.off_bq_w);
+      const uint32_t kbd = BQT ? (uint32_t)P.kb_buf >> 4 : 0u;
       const uint64_t dv = sdesc_mn_sw128(smem + P.off_v), dvt = sdesc_mn_sw32(smem + P.off_v_t);
       auto issue_s = [&](int X, int b) {
         const uint64_t q = dq[X] + b * bufd, qt = dqt[X] + b * bufd;
@@ -320,8 +326,13 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) umma_ss(d, q + 2 * ks, kk + k0 * 8 + 2 * ks, id, ks > 0);
           if constexpr (kTail) umma_ss(d, qt, kt + k0 * 2, id, 1);
-          umma_ts(d, bq, kh + k0 * 2, idh, 1);      // + bh[σq, ky] / tau
-          umma_ts(d, bq + 8, kw + k0 * 2, idh, 1);  // + bw[σq, kx] / tau
+          if constexpr (BQT) {
+            umma_ts(d, bq, kh + k0 * 2, idh, 1);      // + bh[σq, ky] / tau
+            umma_ts(d, bq + 8, kw + k0 * 2, idh, 1);  // + bw[σq, kx] / tau
+          } else {  // Bq slabs: tile B rows start at row 128 (x 32 B)
+            umma_ss(d, dbh + X * 256, kh + k0 * 2, idh, 1);
+            umma_ss(d, dbw + X * 256, kw + k0 * 2, idh, 1);
+          }
         }
         umma_commit_elect(&s_full[X]);
       };
@@ -342,6 +353,15 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         }
         umma_commit_elect(&o_full[X]);
       };
+      // bias operands of item k in place (key rows; BQT: tile X's Bq rows in TMEM)
+      auto wait_bias = [&](int k_, int X) {
+        if constexpr (BQT) {
+          mbar_wait(&bk_full[k_ & 1], (k_ >> 1) & 1);
+          mbar_wait(&bq_full[X], k_ & 1);
+        } else {
+          mbar_wait(bk_full, k_ & 1);
+        }
+      };
       int k = 0, pb = 0;
       if (P.seq) {
         // high densities (S_A + S_B + 2 O > 512 columns): the two tiles share the S columns and run
@@ -350,19 +370,18 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
           const int b = k & 1;
           mbar_wait(&qk_full[b], (k >> 1) & 1);
-          mbar_wait(&bk_full[b], (k >> 1) & 1);
-          mbar_wait(&bq_full[0], k & 1);
+          wait_bias(k, 0);
           tc_fence_after();
           issue_s(0, b);
           mbar_wait_sleep(&p_full[0], k & 1);
           mbar_wait(&v_full[b], (k >> 1) & 1);
           tc_fence_after();
           issue_pv(0, b);
-          mbar_wait(&bq_full[1], k & 1);
+          if constexpr (BQT) mbar_wait(&bq_full[1], k & 1);
           tc_fence_after();
           issue_s(1, b);
           umma_commit_elect(&qk_empty[b]);
-          umma_commit_elect(&bk_empty[b]);
+          umma_commit_elect(&bk_empty[BQT ? b : 0]);
           mbar_wait_sleep(&p_full[1], k & 1);
           tc_fence_after();
           issue_pv(1, b);
@@ -372,8 +391,7 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
       for (int it = P.seq ? P.items : blockIdx.x; it < P.items; it += gridDim.x, ++k) {
         const int b = k & 1;
         mbar_wait(&qk_full[b], (k >> 1) & 1);
-        mbar_wait(&bk_full[b], (k >> 1) & 1);
-        mbar_wait(&bq_full[0], k & 1);
+        wait_bias(k, 0);
         tc_fence_after();
         issue_s(0, b);
         if (lane == 0) ZS_TR(k, 2);
@@ -385,13 +403,13 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
             umma_commit_elect(&v_empty[pb]);
             if (lane == 0) ZS_TR(k, 3);
           }
-          mbar_wait(&bq_full[1], k & 1);
+          if constexpr (BQT) mbar_wait(&bq_full[1], k & 1);
           tc_fence_after();
           issue_s(1, b);
           if (lane == 0) ZS_TR(k, 4);
         }
         umma_commit_elect(&qk_empty[b]);
-        umma_commit_elect(&bk_empty[b]);
+        umma_commit_elect(&bk_empty[BQT ? b : 0]);
         mbar_wait_sleep(&p_full[0], k & 1);
         mbar_wait(&v_full[b], (k >> 1) & 1);
         tc_fence_after();
@@ -407,6 +425,7 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         umma_commit_elect(&v_empty[pb]);
       }
     } else {
+      if constexpr (BQT) {
       // ---------------------------------------------------------- one-hot key rows of each item
       // kb1[σk(j)] = e_{σk/w} | e_{σk%w} (two 16-column SW32 slabs), 64-byte-row gathers with
       // 16-byte cp.async (8 rows x 4 chunks per instruction); warp 2 rows [0, 128), warp 3 the
@@ -450,6 +469,52 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
           mbar_arrive(&bk_full[b]);
           if (warp == 2) ZS_TR(k, 8);
         }
+      }
+      } else {
+      // Bq rows btab[h, σq(r)] (warp 3) and one-hot key rows kb1[σk(j)] (warp 2) into single
+      // shared-memory buffers, 64-byte-row gathers with 16-byte cp.async
+      const bool is_q = warp == 3;
+      const int nrows = is_q ? P.S : P.kv_rows;
+      const uint32_t off_h = is_q ? P.off_bq_h : P.off_kb_h, off_w = is_q ? P.off_bq_w : P.off_kb_w;
+      const int c = lane & 3;
+      uint8_t* slab = smem + ((c >> 1) ? off_w : off_h);
+      int k = 0;
+      for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
+        const int u = it / P.heads, h = it % P.heads;
+        const int* isrc = (is_q ? P.q_sp : P.k_sp) + (long long)u * P.S;
+        int idx[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int j = lane + 32 * i;
+          idx[i] = j < P.S ? __ldg(isrc + j) : -1;
+        }
+        const __half* tab = is_q ? P.btab + (long long)u * P.btab_us + (long long)h * P.S * 32 : P.kb1;
+        mbar_wait_sleep(bk_empty, (k & 1) ^ 1);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (32 * i >= nrows) break;
+#pragma unroll
+          for (int l = 0; l < 32; l += 8) {
+            const int rl = l + (lane >> 2);
+            const int r = 32 * i + rl;
+            const int sp = __shfl_sync(0xffffffffu, idx[i], rl);
+            if (r < nrows) {
+              uint8_t* dst = slab + sw32_off(r, c & 1);
+              if (sp >= 0)
+                cp_async16(dst, tab + (long long)sp * 32 + c * 8);
+              else
+                *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);  // key rows past S
+            }
+          }
+        }
+        cp_async_wait_all();
+        fence_proxy_async_smem();  // generic-proxy smem writes -> tensor core
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(bk_full);
+          if (is_q) ZS_TR(k, 8);
+        }
+      }
       }
     }
   } else {
@@ -561,7 +626,7 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
     };
     uint4 bqn[4];
     int spn = -1;
-    if (warp_live && blockIdx.x < P.items) {
+    if (BQT && warp_live && blockIdx.x < P.items) {
       load_bq(blockIdx.x, load_sp(blockIdx.x), bqn);
       store_bq(bqn);                                       // item 0
       load_bq(blockIdx.x + G, load_sp(blockIdx.x + G), bqn);  // item 1, in flight during item 0
@@ -575,7 +640,7 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         const int om = out_row(it);
         mbar_wait(&s_full[X], k & 1);
         tc_fence_after();
-        if (it + G < P.items) {  // S'(k) done reading Bq(k): install Bq(k + 1)
+        if (BQT && it + G < P.items) {  // S'(k) done reading Bq(k): install Bq(k + 1)
           store_bq(bqn);
           load_bq(it + 2 * G, spn, bqn);
           spn = load_sp(it + 3 * G);
@@ -738,16 +803,21 @@ int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, 
   }
   const int wa = (p.s_col[0] + 31) & ~31, wb = p.s_col[1];
   p.seq = 0;
-  // TMEM: S columns | Bq (2 x 16) | O_A | O_B (96 wide when they fit, else 80)
+  // TMEM: S columns | Bq (2 x 16, BQT) | O_A | O_B (96 wide when they fit, else 80)
+  bool bqt = true;
   if (wa + wb + 32 + 2 * 80 > (int)kTmemCols) {
-    // high density: tiles A and B one after the other over shared S columns
-    if (p.nt < 2 || std::max(wa, wb) + 32 + 2 * 80 > (int)kTmemCols || getenv("ZS_WIN_NO_SEQ")) return 1;
-    p.seq = 1;
+    if (wa + wb + 2 * 80 <= (int)kTmemCols) {
+      bqt = false;  // Bq rows in shared memory instead
+    } else {
+      // high density: tiles A and B one after the other over shared S columns
+      if (p.nt < 2 || std::max(wa, wb) + 32 + 2 * 80 > (int)kTmemCols || getenv("ZS_WIN_NO_SEQ")) return 1;
+      p.seq = 1;
+    }
   }
   p.s_col[0] = 0;
   p.s_col[1] = p.seq ? 0 : wa;
   const int s_cols = p.seq ? std::max(wa, wb) : wa + wb;
-  if (s_cols + 32 <= (int)kTmemCols - 2 * 96) {  // O accumulators 32-column aligned when they fit
+  if (s_cols + (bqt ? 32 : 0) <= (int)kTmemCols - 2 * 96) {  // O accumulators 32-column aligned when they fit
     p.o_col[0] = (int)kTmemCols - 2 * 96;
     p.o_col[1] = (int)kTmemCols - 96;
   } else {
@@ -789,11 +859,22 @@ int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, 
   if (tail) off = std::max(off, p.off_qb_t + 128 * 32);
   p.buf_bytes = (off + 1023) / 1024 * 1024;
   off = 2 * p.buf_bytes;
-  // one-hot key rows, two buffers: [kb_h | kb_w] of buffer 0, then of buffer 1
-  p.off_kb_h = take(kvs * 32, 1024);
-  p.off_kb_w = take(kvs * 32, 256);
-  p.kb_buf = (off - p.off_kb_h + 1023) / 1024 * 1024;
-  off = p.off_kb_h + 2 * p.kb_buf;
+  if (bqt) {
+    // one-hot key rows, two buffers: [kb_h | kb_w] of buffer 0, then of buffer 1
+    p.off_bq_h = p.off_bq_w = 0;
+    p.off_kb_h = take(kvs * 32, 1024);
+    p.off_kb_w = take(kvs * 32, 256);
+    p.kb_buf = (off - p.off_kb_h + 1023) / 1024 * 1024;
+    off = p.off_kb_h + 2 * p.kb_buf;
+  } else {
+    // Bq slabs: tile A rows [0,128) then tile B rows (the MMA reads 128 rows from 128*32); one
+    // key-row buffer
+    p.off_bq_h = take(256 * 32, 1024);
+    p.off_bq_w = take(256 * 32, 1024);
+    p.off_kb_h = take(kvs * 32, 256);
+    p.off_kb_w = take(kvs * 32, 256);
+    p.kb_buf = 0;
+  }
   p.off_bar = take(256, 8);
   const size_t smem = 1024 + (size_t)off;
   if (smem > 227 * 1024) return 1;
@@ -846,11 +927,21 @@ int launch_attn_win(const void* q, const void* k, const void* v, long long ldq, 
     { kern<<<grid, kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], m[6], m[7], m[8], m[9], m[10], m[11], p); count_launch(); }
   };
   if (dh == 64) {
-    if (reg) launch(zs_attn_win_kernel<64, true>);
-    else launch(zs_attn_win_kernel<64, false>);
+    if (bqt) {
+      if (reg) launch(zs_attn_win_kernel<64, true, true>);
+      else launch(zs_attn_win_kernel<64, false, true>);
+    } else {
+      if (reg) launch(zs_attn_win_kernel<64, true, false>);
+      else launch(zs_attn_win_kernel<64, false, false>);
+    }
   } else {
-    if (reg) launch(zs_attn_win_kernel<80, true>);
-    else launch(zs_attn_win_kernel<80, false>);
+    if (bqt) {
+      if (reg) launch(zs_attn_win_kernel<80, true, true>);
+      else launch(zs_attn_win_kernel<80, false, true>);
+    } else {
+      if (reg) launch(zs_attn_win_kernel<80, true, false>);
+      else launch(zs_attn_win_kernel<80, false, false>);
+    }
   }
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }
