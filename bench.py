@@ -686,7 +686,7 @@ def kernel_report(kern: dict, steps: int, peaks: dict):
         pass
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": achieved / peak_tf if peak_tf else None, "traffic": traffic,
-                "traffic_source": "ncu --set full of `bench.py --profile` (profiles/ncu_summary.json)",
+                "traffic_source": "ncu --set full of one bench-config forward (tools/prof_step.py; profiles/ncu_summary.json)",
                 "traffic_by_kernel": by_kernel, "kernel": "zs_gemm2_kernel (cta_group::2)",
                 "launches_per_step": gk["launches"] // max(steps, 1), "peak_source": peak_src}
     total = sum(v["ms"] for v in kern.values()) / max(steps, 1)
