@@ -17,13 +17,14 @@
 namespace zs {
 
 namespace order {
-constexpr int TY = 8, TX = 32;       // output pixels per CTA
+constexpr int TY = 10, TX = 24;      // output pixels per CTA (70 x 70 padded grid: 3 % idle)
+constexpr int kThreads = TY * TX;
 constexpr int HY = TY + 2, HX = TX + 2;
 constexpr int CC = 16;               // channels staged per pass
 constexpr int CCP = CC + 1;          // padded channel stride (bank-conflict free)
 }  // namespace order
 
-__global__ void __launch_bounds__(256) sobel_kernel(const float* __restrict__ x, int H, int W, int C, int win,
+__global__ void __launch_bounds__(order::kThreads) sobel_kernel(const float* __restrict__ x, int H, int W, int C, int win,
                                                     int Hp, int Wp, int nwx, float* __restrict__ sal_glob,
                                                     float* __restrict__ sal_win) {
   using namespace order;
@@ -35,27 +36,31 @@ __global__ void __launch_bounds__(256) sobel_kernel(const float* __restrict__ x,
   const float* xb = x + (long long)b * H * W * C;
 
   float gxg = 0.f, gyg = 0.f, gxw = 0.f, gyw = 0.f;
-  // neighbour (dy,dx) in {-1,0,1}: inside-window / inside-grid masks for this pixel
-  bool in_g[3][3], in_w[3][3];
+  // Taps outside the grid read the zero-filled halo, so they add +-0 exactly like the
+  // reference's zero padding (a zero addend changes only the sign of a zero accumulator, which
+  // the magnitude squares away); the global map needs no masks.  The window map also drops the
+  // taps outside the pixel's window: their values are ANDed with a per-tap bit mask (integer
+  // pipe, no predicates per tap and channel), which turns them into +0.
+  const bool rok0 = (py % win) != 0, rok2 = (py % win) != win - 1;
+  const bool cok0 = (px % win) != 0, cok2 = (px % win) != win - 1;
+  uint32_t mw[3][3];
 #pragma unroll
   for (int a = 0; a < 3; ++a)
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      const int ny = py + a - 1, nx = px + c - 1;
-      const bool grid_ok = ny >= 0 && nx >= 0 && ny < H && nx < W;
-      in_g[a][c] = grid_ok;
-      in_w[a][c] = grid_ok && (ny / win == py / win) && (nx / win == px / win) && ny >= 0 && nx >= 0;
+      const bool ra = a == 0 ? rok0 : (a == 2 ? rok2 : true), cc = c == 0 ? cok0 : (c == 2 ? cok2 : true);
+      mw[a][c] = (ra && cc) ? 0xffffffffu : 0u;
     }
 
   // halo staging, software-pipelined: the 16-byte loads of pass c0 + CC are in flight (in
   // registers) while pass c0 is computed from shared memory
-  constexpr int NLD = (HY * HX * (CC / 4) + 255) / 256;
+  constexpr int NLD = (HY * HX * (CC / 4) + kThreads - 1) / kThreads;
   const bool vec = (C & 3) == 0 && (C % CC) == 0;
   float4 pre[NLD];
   auto load_pass = [&](int c0) {
 #pragma unroll
     for (int k = 0; k < NLD; ++k) {
-      const int e = threadIdx.x + 256 * k;
+      const int e = threadIdx.x + kThreads * k;
       pre[k] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (e < HY * HX * (CC / 4)) {
         const int q = e % (CC / 4), pp = e / (CC / 4);
@@ -71,7 +76,7 @@ __global__ void __launch_bounds__(256) sobel_kernel(const float* __restrict__ x,
     if (vec) {
 #pragma unroll
       for (int k = 0; k < NLD; ++k) {
-        const int e = threadIdx.x + 256 * k;
+        const int e = threadIdx.x + kThreads * k;
         if (e < HY * HX * (CC / 4)) {
           float* t = tile + (e / (CC / 4)) * CCP + 4 * (e % (CC / 4));
           t[0] = pre[k].x;
@@ -81,7 +86,7 @@ __global__ void __launch_bounds__(256) sobel_kernel(const float* __restrict__ x,
         }
       }
     } else {
-      for (int e = threadIdx.x; e < HY * HX * CC; e += 256) {
+      for (int e = threadIdx.x; e < HY * HX * CC; e += kThreads) {
         const int ch = e % CC;
         const int p = e / CC;
         const int hy = p / HX, hx = p % HX;
@@ -100,27 +105,31 @@ __global__ void __launch_bounds__(256) sobel_kernel(const float* __restrict__ x,
       for (int a = 0; a < 3; ++a)
 #pragma unroll
         for (int c = 0; c < 3; ++c) v[a][c] = tile[((ty + a) * HX + (tx + c)) * CCP + ch];
-      // global map: taps row-major; gx uses (0,0),(0,2),(1,0),(1,2),(2,0),(2,2); gy rows 0 and 2
-// coef * v is exact for coef in {+-1, +-2}, so the single-rounding fma equals the reference's
-// separately rounded multiply-then-add bit for bit, at half the instructions
-#define ZS_TAP(acc, mask, a, c, coef) \
-  if (mask[a][c]) acc = __fmaf_rn(coef, v[a][c], acc);
-      ZS_TAP(gxg, in_g, 0, 0, -1.f) ZS_TAP(gyg, in_g, 0, 0, -1.f)
-      ZS_TAP(gyg, in_g, 0, 1, -2.f)
-      ZS_TAP(gxg, in_g, 0, 2, 1.f) ZS_TAP(gyg, in_g, 0, 2, -1.f)
-      ZS_TAP(gxg, in_g, 1, 0, -2.f)
-      ZS_TAP(gxg, in_g, 1, 2, 2.f)
-      ZS_TAP(gxg, in_g, 2, 0, -1.f) ZS_TAP(gyg, in_g, 2, 0, 1.f)
-      ZS_TAP(gyg, in_g, 2, 1, 2.f)
-      ZS_TAP(gxg, in_g, 2, 2, 1.f) ZS_TAP(gyg, in_g, 2, 2, 1.f)
-      ZS_TAP(gxw, in_w, 0, 0, -1.f) ZS_TAP(gyw, in_w, 0, 0, -1.f)
-      ZS_TAP(gyw, in_w, 0, 1, -2.f)
-      ZS_TAP(gxw, in_w, 0, 2, 1.f) ZS_TAP(gyw, in_w, 0, 2, -1.f)
-      ZS_TAP(gxw, in_w, 1, 0, -2.f)
-      ZS_TAP(gxw, in_w, 1, 2, 2.f)
-      ZS_TAP(gxw, in_w, 2, 0, -1.f) ZS_TAP(gyw, in_w, 2, 0, 1.f)
-      ZS_TAP(gyw, in_w, 2, 1, 2.f)
-      ZS_TAP(gxw, in_w, 2, 2, 1.f) ZS_TAP(gyw, in_w, 2, 2, 1.f)
+      float u[3][3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) u[a][c] = __uint_as_float(__float_as_uint(v[a][c]) & mw[a][c]);
+      // taps row-major; gx uses (0,0),(0,2),(1,0),(1,2),(2,0),(2,2); gy rows 0 and 2.  coef * v is
+      // exact for coef in {+-1, +-2}, so the single-rounding fma equals the reference's separately
+      // rounded multiply-then-add bit for bit
+#define ZS_TAP(acc, vv, a, c, coef) acc = __fmaf_rn(coef, vv[a][c], acc);
+      ZS_TAP(gxg, v, 0, 0, -1.f) ZS_TAP(gyg, v, 0, 0, -1.f)
+      ZS_TAP(gyg, v, 0, 1, -2.f)
+      ZS_TAP(gxg, v, 0, 2, 1.f) ZS_TAP(gyg, v, 0, 2, -1.f)
+      ZS_TAP(gxg, v, 1, 0, -2.f)
+      ZS_TAP(gxg, v, 1, 2, 2.f)
+      ZS_TAP(gxg, v, 2, 0, -1.f) ZS_TAP(gyg, v, 2, 0, 1.f)
+      ZS_TAP(gyg, v, 2, 1, 2.f)
+      ZS_TAP(gxg, v, 2, 2, 1.f) ZS_TAP(gyg, v, 2, 2, 1.f)
+      ZS_TAP(gxw, u, 0, 0, -1.f) ZS_TAP(gyw, u, 0, 0, -1.f)
+      ZS_TAP(gyw, u, 0, 1, -2.f)
+      ZS_TAP(gxw, u, 0, 2, 1.f) ZS_TAP(gyw, u, 0, 2, -1.f)
+      ZS_TAP(gxw, u, 1, 0, -2.f)
+      ZS_TAP(gxw, u, 1, 2, 2.f)
+      ZS_TAP(gxw, u, 2, 0, -1.f) ZS_TAP(gyw, u, 2, 0, 1.f)
+      ZS_TAP(gyw, u, 2, 1, 2.f)
+      ZS_TAP(gxw, u, 2, 2, 1.f) ZS_TAP(gyw, u, 2, 2, 1.f)
 #undef ZS_TAP
     }
   }
@@ -228,7 +237,7 @@ extern "C" int zs_sobel_saliency(const float* x, int B, int H, int W, int C, int
   const int Hp = (H + window - 1) / window * window, Wp = (W + window - 1) / window * window;
   const int nwx = Wp / window;
   dim3 grid((Wp + order::TX - 1) / order::TX, (Hp + order::TY - 1) / order::TY, B);
-  { sobel_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(x, H, W, C, window, Hp, Wp, nwx,
+  { sobel_kernel<<<grid, order::kThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(x, H, W, C, window, Hp, Wp, nwx,
                                                                           sal_glob, sal_win); count_launch(); }
   return cudaGetLastError() == cudaSuccess ? 0 : ZS_ERR_LAUNCH;
 }

@@ -1,2 +1,2 @@
-ZS_AB_LIBS=libzstripe_b200.so,libzstripe_b200_old.so,libzstripe_b200_lsuout.so,libzstripe_b200_skipout.so timeout 300 python tools/attn_ab.py local 64 2>&1 | grep -A1 median
-ZS_AB_LIBS=libzstripe_b200.so,libzstripe_b200_old.so,libzstripe_b200_lsuout.so timeout 300 python tools/attn_ab.py local 64 rows 2>&1 | grep -A1 median
+timeout 120 python tools/sobel_ab.py
+timeout 300 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_api.py -q -x -k "sobel or order or saliency" --timeout 120 2>&1 | tail -2
