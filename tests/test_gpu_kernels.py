@@ -343,6 +343,14 @@ def test_attention_many_items_per_cta(dh):
     assert _attn_case(5, 8, 4096, dh, 64, 128, 0.4, seed=2) < 1e-2
 
 
+@pytest.mark.parametrize("r", [0.2, 0.6, 0.8])
+def test_attention_window_variants_many_items(r):
+    """The window kernel's three schedules with several items per CTA: Bq rows in TMEM with
+    double-buffered key rows (d = 0.2), shared-memory Bq slabs (d = 0.6: S_A + S_B + 2 O fill the
+    TMEM columns), tiles in sequence (d = 0.8)."""
+    assert _attn_case(300, 2, 196, 80, 14, 32, r, seed=12) < 1e-2
+
+
 def test_attention_general_tiles_many_items():
     """Tile sizes that are not multiples of 32 take the per-element mask path."""
     g = torch.Generator().manual_seed(9)
