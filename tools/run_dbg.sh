@@ -1,2 +1,2 @@
-timeout 120 python tools/sobel_ab.py
-timeout 300 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_api.py -q -x -k "sobel or order or saliency" --timeout 120 2>&1 | tail -2
+timeout 300 python -m pytest tests/test_gpu_kernels.py -q -x -k "gemm or mlp" --timeout 120 2>&1 | tail -2
+timeout 400 python tools/gemm_ab.py 48 proj,fc2 2>&1 | tail -2
