@@ -1,2 +1,1 @@
-timeout 300 python -m pytest tests/test_gpu_kernels.py -q -x -k "gemm or mlp" --timeout 120 2>&1 | tail -2
-timeout 400 python tools/gemm_ab.py 48 proj,fc2 2>&1 | tail -2
+ZS_AB_LIBS=libzstripe_b200.so,libzstripe_b200_old.so,libzstripe_b200_p1.so,libzstripe_b200_p2.so,libzstripe_b200_p3.so timeout 300 python tools/attn_ab.py local 64 2>&1 | grep -A1 median
