@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         const uint64_t kh = dkh + b * kbd, kw = dkw + b * kbd;
         const uint32_t bq = tmem + P.tm_bq + 16 * X;  // A operand: this tile's [bh | bw] rows (fp16)
         const uint32_t d0 = tmem + P.s_col[X];
+#pragma unroll 1  // not unrolled: the kernel is instruction-cache bound
         for (int r = 0; r < P.nrun[X]; ++r) {
           const int k0 = P.run_k0[X][r], n = P.run_n[X][r];
           const uint32_t id = idesc_bf16(128, n), idh = idesc_f16(128, n);
@@ -341,6 +342,7 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
         const uint32_t a0 = tmem + P.s_col[X];
         const uint32_t d = tmem + P.o_col[X];
         uint32_t acc = 0;
+#pragma unroll 1  // not unrolled: the kernel is instruction-cache bound
         for (int r = 0; r < P.nrun[X]; ++r) {
           const int k0 = P.run_k0[X][r], n = P.run_n[X][r], c0 = P.run_c0[X][r];
           for (int s = 0; s < n / 16; ++s) {
