@@ -111,10 +111,11 @@ __device__ __forceinline__ void tmem_ld_group(uint32_t taddr, uint32_t* r, bool 
   tmem_ld16p(taddr, r);
   if (w32) tmem_ld16p(taddr + 16, r + 16);
 }
-// row max of one key group (keys past S -> -inf first); W = width in S columns, vc = keys below S
-template <int W>
+// row max of one key group; W = width in S columns, vc = keys below S.  MASK: keys past S -> -inf
+// first (without it, keys past S carry the -30000 bias marker, see the BQT key-row gather)
+template <int W, bool MASK>
 __device__ __forceinline__ float group_max(uint32_t* sr, int vc) {
-  if (vc < W) {
+  if (MASK && vc < W) {
 #pragma unroll
     for (int j = 0; j < W; ++j)
       if (j >= vc) sr[j] = __float_as_uint(-INFINITY);
@@ -435,6 +436,11 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
       const int i0 = (warp - 2) * 4;
       const int nrows = P.kv_rows;
       const int c = lane & 3;
+      // key rows past S get fp16 1.0 in bias column 15 (free when w < 16: one-hot columns are
+      // ky, kx < w), which the Bq rows hold as -30000: S' of those keys is ~-30000 and their P
+      // underflows to exactly 0, so the softmax needs no key-range masking.  (w = 16 means
+      // S = 256: no keys past S.)
+      const uint4 kmark = (c == 1 && P.bias_w < 16) ? make_uint4(0u, 0u, 0u, 0x3C000000u) : make_uint4(0u, 0u, 0u, 0u);
       int k = 0;
       for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
         const int u = it / P.heads, b = k & 1;
@@ -460,7 +466,7 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
               if (sp >= 0)
                 cp_async16(dst, P.kb1 + (long long)sp * 32 + c * 8);
               else
-                *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);  // key rows past S
+                *reinterpret_cast<uint4*>(dst) = kmark;  // key rows past S: the bias marker column
             }
           }
         }
@@ -581,7 +587,7 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
     };
     auto gmax = [&](int g, uint32_t* sr) -> float {
       const int vc = P.S - 32 * g;
-      return P.gw[g] == 32 ? group_max<32>(sr, vc) : group_max<16>(sr, vc);
+      return P.gw[g] == 32 ? group_max<32, !BQT>(sr, vc) : group_max<16, !BQT>(sr, vc);
     };
     auto emit_p = [&](int g, const uint32_t* sr, float mc, float& rs) {
       const uint32_t pa = s_addr + (uint32_t)(P.gcol[X][g] >> 1);
@@ -614,7 +620,8 @@ __global__ void __launch_bounds__(attnw::kThreads, 1)
                        : "memory");
       }
     };
-    auto store_bq = [&](const uint4 (&x)[4]) {
+    auto store_bq = [&](uint4 (&x)[4]) {
+      if (P.bias_w < 16) x[1].w = (x[1].w & 0xffffu) | 0xF7530000u;  // column 15: fp16 -30000 (marker)
       asm volatile(
           "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
           "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(bq_addr),
