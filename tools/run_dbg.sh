@@ -1,1 +1,2 @@
-ZS_AB_LIBS=libzstripe_b200.so,libzstripe_b200_old.so,libzstripe_b200_p1.so,libzstripe_b200_p2.so,libzstripe_b200_p3.so timeout 300 python tools/attn_ab.py local 64 2>&1 | grep -A1 median
+timeout 300 python -m pytest tests/test_gpu_kernels.py -q -x -k "attention_local or window" --timeout 120 2>&1 | tail -2
+timeout 300 python tools/attn_ab.py local 64 2>&1 | grep -A1 median
