@@ -73,6 +73,7 @@ struct Params {
   int off_q, off_k, off_oh, off_v, off_ml, off_ost, off_bar, tile, vstage;
   int tma_out;  // 1: the O tile leaves through shared memory and one TMA tensor store (no o_rows)
   int trace;
+  uint32_t w_magic;  // floor(2^32 / bias_w) + 1: s / bias_w == umulhi(s, w_magic) for s < 2^32 / bias_w
 };
 
 template <int DH>
@@ -447,7 +448,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
             prev[sidx][e][0] = prev[sidx][e][1] = -1;
             const int sp = spc[e];
             if (sp >= 0) {
-              const int ky = sp / P.bias_w, kx = sp % P.bias_w;
+              const int ky = (int)__umulhi((uint32_t)sp, P.w_magic), kx = sp - ky * P.bias_w;
               const int oy = kr * 128 + (((ky >> 3) ^ (kr & 7)) << 4);
               const int ox = BQ * 128 + kr * 128 + (((kx >> 3) ^ (kr & 7)) << 4);
               const uint32_t vy = one << (16 * (ky & 1)), vx = one << (16 * (kx & 1));
@@ -774,6 +775,7 @@ int launch_attn_glob(const void* q, const void* k, const void* v, long long ldq,
   p.tau = tau;
   p.out = reinterpret_cast<__nv_bfloat16*>(out);
   p.trace = getenv("ZS_GLOB_TRACE") ? 1 : 0;
+  p.w_magic = (uint32_t)((1ull << 32) / (unsigned)bias_w + 1ull);
   const int tile = dh == 80 ? Shape<80>::TILE : Shape<64>::TILE;
   p.tile = tile;
   p.vstage = dh == 80 ? Shape<80>::VSTAGE : Shape<64>::VSTAGE;
