@@ -285,11 +285,12 @@ def test_attention_local_window(dh, r):
 
 
 @pytest.mark.parametrize("S,w,tile,r", [(100, 10, 32, 0.4), (144, 12, 32, 0.5), (225, 15, 64, 0.3), (64, 8, 32, 1.0),
-                                        (121, 11, 32, 0.4), (169, 13, 32, 0.5)])
+                                        (121, 11, 32, 0.4), (169, 13, 32, 0.5), (256, 16, 32, 0.4)])
 def test_attention_window_shapes(S, w, tile, r):
     """Single-tile windows (S <= 128), a 144-token window, 64-row tiles, odd table widths; partial
     last key groups (32 wide with 25 keys for S = 121, 16 wide with 9 keys for S = 169), which the
-    kernel masks with the bias marker column rather than per element."""
+    kernel masks with the bias marker column rather than per element; S = 256 (w = 16: no free
+    bias column, and no keys past S)."""
     assert _attn_case(7, 3, S, 80, w, tile, r, seed=3) < 1e-2
     assert _attn_case(7, 2, S, 64, w, tile, r, seed=4) < 1e-2
 
