@@ -23,8 +23,14 @@
 //    Q_B rows, which only produce discarded output rows.
 //  * MMA issue order ping-pongs the two softmax warpgroups:
 //      S_A(k) PV_B(k-1) S_B(k) PV_A(k) S_A(k+1) ...
-// Roles: warp 0 TMA, warp 1 MMA, warps 2-3 bias operands by 16-byte cp.async (warp 3: fp16 bias
-// rows by σq, warp 2: one-hot key rows by σk; warp 2 also owns the TMEM allocation), warps 4-7
+//  * Bias operands off the MMA chain (BQT variant): each query row's Bq (32 fp16) is written into
+//    TMEM by the row's own softmax thread for item k + 1 as soon as S'(k) completed (A operand of
+//    TS bias MMAs); the one-hot key rows are double-buffered and gathered one item ahead; keys past
+//    S carry a -30000 bias marker column instead of being masked per element.  When those 32 TMEM
+//    columns do not fit (d ~ 0.55-0.75), Bq lives in shared-memory slabs (BQT = false).
+//  * The kernel is instruction-cache sensitive: loops over runtime schedule sizes stay rolled.
+// Roles: warp 0 TMA, warp 1 MMA, warps 2-3 one-hot key rows by 16-byte cp.async (BQT = false:
+// warp 3 the Bq rows, warp 2 the key rows; warp 2 also owns the TMEM allocation), warps 4-7
 // softmax tile A, warps 8-11 softmax tile B (one thread per row; exponentials on the packed fp32
 // pipes, exp2_pair_bf16 in zs_common.cuh).
 #include <cuda_fp16.h>
