@@ -29,12 +29,14 @@
 //    Q tiles are loaded by their own producer lane (the K / V rings run ahead into the next
 //    item), and the MMA stream runs across items (the next item's first S' before this item's
 //    last PV): at an item boundary only the last PV and the epilogue remain serial.
-//  * Epilogue: the O tile is packed to bf16 in shared memory and leaves through one TMA tensor
-//    store per item (16-byte stores to 128 scattered rows held the softmax warps ~3000 cycles).
-//    TMEM: S 256 + O_0 96 + O_1 96 + Bq 64 = 512 columns.  An item's epilogue runs after the
-//    next item's first chunk, when its last PVs have long completed.
+//  * Epilogue on its own warps (12-15, one per TMEM lane quarter): when both halves published
+//    their final reference maxima and the item's last PVs completed, they read O_0 / O_1 and the
+//    row sums, free the accumulators for the next item's first PV, merge the halves and write the
+//    tile through shared memory and one TMA tensor store per item, while the softmax warps are
+//    already in the next item.  TMEM: S 256 + O_0 96 + O_1 96 + Bq 64 = 512 columns.
 // Roles: warp 0 TMA (lane 0: Q per item + K per chunk, lane 1: V per chunk), warp 1 MMA (whole
-// warp, elected lane), warps 2-3 one-hot key rows per chunk, warps 4-11 softmax.
+// warp, elected lane), warps 2-3 one-hot key rows per chunk, warps 4-11 softmax, warps 12-15
+// epilogue (registers 96 / 152 / 112 per warpgroup through setmaxnreg).
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -47,7 +49,7 @@ namespace zs {
 namespace attng {
 
 constexpr int BQ = 128;
-constexpr int kThreads = 384;
+constexpr int kThreads = 512;  // 4 producer / MMA / one-hot warps, 8 softmax warps, 4 epilogue warps
 constexpr uint32_t kTmemCols = 512;
 constexpr int KST = 3;  // K ring stages
 constexpr int OST = 2;  // one-hot ring stages (generated on chip: no memory latency to hide)
@@ -155,6 +157,109 @@ __device__ unsigned long long g_glob_trace2[128];
   } while (0)
 #endif
 
+// Epilogue warps (12-15) of zs_attn_glob_kernel: warp 12 + q owns rows [32q, 32q + 32) of every
+// item (TMEM lane quarter q).  See the role comment in the kernel.
+template <int DH>
+__device__ __forceinline__ void epilogue_warps(const attng::Params& P, uint8_t* smem, uint32_t tmem, uint64_t* m_full,
+                                               uint64_t* o_last, uint64_t* o_free, const CUtensorMap& to,
+                                               const CUtensorMap& to_t, int q, int lane, int nmb) {
+  using namespace attng;
+  using L = Shape<DH>;
+  constexpr bool kTail = L::kTail;
+  constexpr float L2E = 1.4426950408889634f;
+  constexpr int NC = DH / 8;  // 16-byte pieces of an output row
+  const int r = q * 32 + lane;
+  const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+  const float* xch = reinterpret_cast<const float*>(smem + P.off_ml);  // [item parity][half][BQ]
+  const bool issuer = q == 0 && lane == 0;
+  uint8_t* st = smem + P.off_ost;
+  int k = 0;
+  for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
+    const int i = it % nmb, uh = it / nmb, h = uh % P.heads, u = uh / P.heads;
+    mbar_wait(&m_full[k & 1], (k >> 1) & 1);
+    const float m0 = xch[(k & 1) * 2 * BQ + r], m1 = xch[(k & 1) * 2 * BQ + BQ + r];
+    const float m = fmaxf(m0, m1);
+    const float a0 = (m0 == -INFINITY) ? 0.f : ex2((m0 - m) * L2E);
+    const float a1 = (m1 == -INFINITY) ? 0.f : ex2((m1 - m) * L2E);
+    mbar_wait(o_last, k & 1);  // the item's last PVs of both halves
+    tc_fence_after();
+    const uint32_t o0 = tmem + TM_O + lane_off, o1 = o0 + TM_OS;
+    uint32_t l01[2];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(l01[0]) : "r"(o0 + DH));
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(l01[1]) : "r"(o1 + DH));
+    uint4 pk[NC];
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int cc = 0; cc < NC; cc += 2) {  // 16 columns of O_0 and O_1 per step
+      uint32_t va[16], vb[16];
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                   : "=r"(va[0]), "=r"(va[1]), "=r"(va[2]), "=r"(va[3]), "=r"(va[4]), "=r"(va[5]), "=r"(va[6]),
+                     "=r"(va[7]), "=r"(va[8]), "=r"(va[9]), "=r"(va[10]), "=r"(va[11]), "=r"(va[12]), "=r"(va[13]),
+                     "=r"(va[14]), "=r"(va[15])
+                   : "r"(o0 + 8 * cc));
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                   : "=r"(vb[0]), "=r"(vb[1]), "=r"(vb[2]), "=r"(vb[3]), "=r"(vb[4]), "=r"(vb[5]), "=r"(vb[6]),
+                     "=r"(vb[7]), "=r"(vb[8]), "=r"(vb[9]), "=r"(vb[10]), "=r"(vb[11]), "=r"(vb[12]), "=r"(vb[13]),
+                     "=r"(vb[14]), "=r"(vb[15])
+                   : "r"(o1 + 8 * cc));
+      tmem_ld_wait();
+      if (cc == 0) {  // the row sums arrived with the first columns
+        const float l = a0 * __uint_as_float(l01[0]) + a1 * __uint_as_float(l01[1]);
+        s0 = a0 / l;
+        s1 = a1 / l;
+      }
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        float f[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          f[e] = __uint_as_float(va[8 * t + e]) * s0 + __uint_as_float(vb[8 * t + e]) * s1;
+        pk[cc + t] = make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(o_free);  // O_0 / O_1 read: the next item's first PVs may start
+    if (P.tma_out) {
+      if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
+      named_bar_sync(7, 128);
+#pragma unroll
+      for (int gc = 0; gc < NC; ++gc) {
+        const int off = gc < 8 ? r * 128 + ((gc ^ (r & 7)) << 4) : L::MAIN + r * 32 + (((gc - 8) ^ ((r >> 2) & 1)) << 4);
+        *reinterpret_cast<uint4*>(st + off) = pk[gc];
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(7, 128);
+      if (issuer) {
+        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                         reinterpret_cast<uint64_t>(&to)), "r"(h * DH), "r"(i * BQ), "r"(u), "r"(smem_u32(st))
+                     : "memory");
+        if constexpr (kTail)
+          asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                           reinterpret_cast<uint64_t>(&to_t)), "r"(h * DH + 64), "r"(i * BQ), "r"(u),
+                       "r"(smem_u32(st + L::MAIN))
+                       : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    } else {
+      const int row = i * BQ + r;
+      bool valid = row < P.S;
+      long long orow_off = (long long)u * P.o_unit_stride + (long long)row * P.ldo;
+      if (valid && P.o_rows) {
+        const int mrow = P.o_rows[(long long)u * P.S + row];
+        valid = mrow >= 0;
+        orow_off = (long long)mrow * P.ldo;
+      }
+      if (valid) {
+        uint4* d4 = reinterpret_cast<uint4*>(P.out + orow_off + h * DH);  // 16-byte aligned
+#pragma unroll
+        for (int gc = 0; gc < NC; ++gc) d4[gc] = pk[gc];
+      }
+    }
+  }
+  if (P.tma_out && issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 template <int DH>
 __global__ void __launch_bounds__(attng::kThreads, 1)
     zs_attn_glob_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tq_t,
@@ -183,6 +288,7 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
   uint64_t* bq_full = bar + 31;  // 8 warps: the item's Bq rows are in TMEM
   uint64_t* bq_free = bar + 32;  // the item's last S' completed (Bq may be replaced)
   uint64_t* oh_empty = bar + 36; // [OST] S' of the chunk done: one-hot stage free
+  uint64_t* m_full = bar + 26;   // [item parity] 8 softmax warps: the item's final reference maxima in smem
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 34);
   static_assert(KST <= 4 && VST <= 4 && QST <= 2 && OST <= 4, "barrier slots");
 
@@ -216,7 +322,9 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
-    mbar_init(o_free, 8);
+    mbar_init(o_free, 4);
+    mbar_init(&m_full[0], 8);
+    mbar_init(&m_full[1], 8);
     mbar_init(bq_full, 8);
     mbar_init(bq_free, 1);
     fence_mbar_init();
@@ -473,8 +581,18 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         j = j2;
       }
     }
+  } else if (warp >= 12) {
+    // ------------------------------------------------------------ epilogue warps (12-15)
+    // Item k's output, off the softmax warps: once both halves published their final reference
+    // maxima (m_full) and the item's last PVs completed (o_last), warp 12 + q reads rows
+    // [32q, 32q + 32) of O_0 / O_1 and the row sums, frees the accumulators (o_free: the next
+    // item's first PV may start), merges the halves out = (a_0 O_0 + a_1 O_1) / (a_0 l_0 +
+    // a_1 l_1) and writes the row through shared memory and one TMA tensor store per item (or
+    // direct stores through o_rows).
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 112;");
+    epilogue_warps<DH>(P, smem, tmem, m_full, o_last, o_free, to, to_t, warp & 3, lane, nmb);
   } else {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 200;");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 152;");
     // ------------------------------------------------------------ softmax warpgroups
     // Half w (warps 4 + 4w .. 7 + 4w) owns key columns [64w, 64w + 64) of every chunk with its own
     // online softmax: reference max m_w, accumulator O_w (+ row sums), P_w -> p_full[buf][w].  The
@@ -489,7 +607,6 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     const uint32_t o_mine = tmem + TM_O + w * TM_OS + lane_off;  // O_w
     const uint32_t bq_addr = tmem + TM_BQ + w * 32 + lane_off;    // this half's 64 fp16 bias columns
     float* xch = reinterpret_cast<float*>(smem + P.off_ml);       // [item parity][half][BQ] reference max
-    const uint32_t pair_bar = 1 + wq;
     constexpr float L2E = 1.4426950408889634f;
     constexpr float kThr = 5.545177444479562f;  // ln 256
     const float tau = P.tau, cexp = P.tau * L2E;
@@ -557,98 +674,6 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
       }
     };
     // output columns [w*OH, w*OH + OH) of this row; OH = DH / 2 (40 or 32)
-    constexpr int OH = DH / 2;
-    constexpr int NQ = OH / 8;  // 16-byte pieces of this half row
-    auto ld_cols = [&](uint32_t a, uint32_t (&v)[OH]) {
-      tmem_ld32(a, *reinterpret_cast<uint32_t(*)[32]>(v));
-      if constexpr (OH == 40)
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(v[32]), "=r"(v[33]), "=r"(v[34]), "=r"(v[35]), "=r"(v[36]), "=r"(v[37]), "=r"(v[38]),
-                       "=r"(v[39])
-                     : "r"(a + 32));
-    };
-
-    // ---- item epilogue: merge the halves, normalise, store this half's output columns
-    auto epilogue = [&](const int k, const int i, const int h, const int u, const float mref) {
-      const int row = i * BQ + r;
-      float* xk = xch + (k & 1) * 2 * BQ;
-      xk[w * BQ + r] = mref;
-      named_bar_sync(pair_bar, 64);
-      const float mo = xk[(w ^ 1) * BQ + r];
-      const float m = fmaxf(mref, mo);
-      const float a_me = (mref == -INFINITY) ? 0.f : ex2((mref - m) * L2E);
-      const float a_ot = (mo == -INFINITY) ? 0.f : ex2((mo - m) * L2E);
-      const float a0 = w == 0 ? a_me : a_ot, a1 = w == 0 ? a_ot : a_me;
-      if (lane == 0 && wq == 0 && w == 0) ZG_TR(k, 13);
-      mbar_wait(o_last, k & 1);  // the item's last PVs of both halves
-      if (lane == 0 && wq == 0 && w == 0) ZG_TR(k, 14);
-      tc_fence_after();
-      const uint32_t o0 = tmem + TM_O + lane_off, o1 = o0 + TM_OS;
-      uint32_t l01[2];
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(l01[0]) : "r"(o0 + DH));
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(l01[1]) : "r"(o1 + DH));
-      uint32_t va[OH], vb[OH];
-      ld_cols(o0 + w * OH, va);
-      ld_cols(o1 + w * OH, vb);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(o_free);  // O_0 / O_1 are in registers: the next item's PVs may start
-      const float l = a0 * __uint_as_float(l01[0]) + a1 * __uint_as_float(l01[1]);
-      const float s0 = a0 / l, s1 = a1 / l;
-      uint4 pk[NQ];
-#pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        float f[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e)
-          f[e] = __uint_as_float(va[8 * q + e]) * s0 + __uint_as_float(vb[8 * q + e]) * s1;
-        pk[q] = make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
-      }
-      if (P.tma_out) {
-        // O tile -> shared memory (the TMA SW128 / SW32 layout of a [128, 64] + [128, 16] box) ->
-        // one TMA tensor store per item: the stores leave through the async proxy instead of
-        // 16-byte LSU stores to 128 scattered rows, which held this warp for ~3000 cycles
-        const bool issuer = warp == 4 && lane == 0;
-        if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
-        named_bar_sync(6, 256);
-        uint8_t* st = smem + P.off_ost;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-          const int gc = (w * OH) / 8 + q;  // 16-byte chunk of the 2 * DH-byte row
-          const int off = gc < 8 ? r * 128 + ((gc ^ (r & 7)) << 4)
-                                 : L::MAIN + r * 32 + (((gc - 8) ^ ((r >> 2) & 1)) << 4);
-          *reinterpret_cast<uint4*>(st + off) = pk[q];
-        }
-        fence_proxy_async_smem();
-        named_bar_sync(6, 256);
-        if (issuer) {
-          asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
-                           reinterpret_cast<uint64_t>(&to)), "r"(h * DH), "r"(i * BQ), "r"(u), "r"(smem_u32(st))
-                       : "memory");
-          if constexpr (kTail)
-            asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
-                             reinterpret_cast<uint64_t>(&to_t)), "r"(h * DH + 64), "r"(i * BQ), "r"(u),
-                         "r"(smem_u32(st + L::MAIN))
-                         : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-      } else {
-        bool valid = row < P.S;
-        long long orow_off = (long long)u * P.o_unit_stride + (long long)row * P.ldo;
-        if (valid && P.o_rows) {
-          const int mrow = P.o_rows[(long long)u * P.S + row];
-          valid = mrow >= 0;
-          orow_off = (long long)mrow * P.ldo;
-        }
-        if (valid) {
-          uint4* d4 = reinterpret_cast<uint4*>(P.out + orow_off + h * DH + w * OH);  // 16-byte aligned
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) d4[q] = pk[q];
-        }
-      }
-      if (lane == 0 && wq == 0) ZG_TR(k, 4 + w);
-    };
 
     const int G = gridDim.x;
     uint4 bqx[8];
@@ -657,8 +682,6 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
     load_bq(blockIdx.x + G, load_sp(blockIdx.x + G), bqx);  // next item's rows, in flight during this item
     int sp_nn = load_sp(blockIdx.x + 2 * G);                  // and the row index of the one after
     int k = 0, c = 0;
-    int kp = -1, ip = 0, hp = 0, up = 0;  // the previous item, whose epilogue is pending
-    float mp = -INFINITY;
     for (int it = blockIdx.x; it < P.items; it += gridDim.x, ++k) {
       const int i = it % nmb, uh = it / nmb, h = uh % P.heads, u = uh / P.heads;
       const int nc = n_chunks(P, i);
@@ -728,16 +751,15 @@ __global__ void __launch_bounds__(attng::kThreads, 1)
         if (lane == 0) mbar_arrive(&p_full[2 * buf + w]);
         if (lane == 0 && wq == 0 && j == 0 && w == 0) ZG_TR(k, 1);
         if (lane == 0 && wq == 0 && w == 0) ZG_T2(k, j, 2);
-        if (j == 0 && kp >= 0) {
-          epilogue(kp, ip, hp, up, mp);
-          kp = -1;
-        }
       }
-      kp = k, ip = i, hp = h, up = u, mp = m_ref;
+      // publish this half's final reference max for the epilogue warps
+      xch[(k & 1) * 2 * BQ + w * BQ + r] = m_ref;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&m_full[k & 1]);
+      (void)h;
+      (void)u;
     }
-    if (kp >= 0) epilogue(kp, ip, hp, up, mp);
   }
-  if (P.tma_out && warp == 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
