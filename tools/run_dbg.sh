@@ -1,2 +1,1 @@
-timeout 240 python -m pytest tests/test_gpu_kernels.py -q -x -k "global or many_items or o_rows or rows" --timeout 60 2>&1 | tail -3
-timeout 200 python tools/attn_ab.py global 16 stripes 2>&1 | grep -A1 median
+ZS_AB_LIBS=libzstripe_b200_old.so,libzstripe_b200_reg160.so timeout 300 python tools/attn_ab.py local 64 2>&1 | grep -A1 median
