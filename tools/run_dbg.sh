@@ -1,1 +1,3 @@
-ZS_AB_LIBS=libzstripe_b200_old.so,libzstripe_b200_reg160.so timeout 300 python tools/attn_ab.py local 64 2>&1 | grep -A1 median
+# scratch gpurun payload used for one-off checks during development (A/B runs, bisects); see the
+# other run_*.sh scripts for the maintained measurement recipes
+timeout 300 python -m pytest tests/test_gpu_kernels.py -q -x --timeout 120 2>&1 | tail -2
