@@ -321,6 +321,14 @@ def test_attention_global(dh, r):
 
 
 @pytest.mark.parametrize("dh", [64, 80])
+def test_attention_global_partial_tiles(dh):
+    """A 30 x 30 grid (S = 900): the last query tile has 4 rows and the last key chunk 4 keys, so
+    the kernel's key-range mask and the epilogue warps' row guard are exercised."""
+    assert _attn_case(3, 2, 900, dh, 30, 128, 0.4, seed=13) < 1e-2
+    assert _attn_case(2, 3, 900, dh, 30, 128, 1.0, seed=14) < 1e-2
+
+
+@pytest.mark.parametrize("dh", [64, 80])
 @pytest.mark.parametrize("r", [0.2, 0.4, 1.0])
 def test_attention_global_parity_stripes(dh, r):
     """Stripe-ordered keys as the global stripe sort produces them (every 128-key chunk inside one
